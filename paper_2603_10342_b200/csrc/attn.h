@@ -1,0 +1,54 @@
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace asb {
+
+// Paged KV cache geometry. One bf16 pool for K and one for V, laid out
+//   [layer][block][kv_head][kBlockTokens][head_dim]
+// so one KV block of one head is a contiguous 64 x head_dim tile (8 or 16 KiB):
+// a single TMA box for prefill attention and a 128-bit-coalesced stream for decode.
+constexpr int kBlockTokens = 64;
+
+// One prefill-attention work item: up to 128 query rows of one segment.
+struct PrefillItem {
+    int q_row0;     // first row in the q / out buffers
+    int q_pos0;     // absolute position of that row
+    int n_q;        // valid query rows (<= 128)
+    int table_off;  // offset of this segment's block table in the batch table array
+};
+
+// One decode-attention row: a single query token.
+struct DecodeItem {
+    int q_row;      // row in q / out
+    int ctx_len;    // keys to attend (positions 0..ctx_len-1), includes the row's own token
+    int table_off;  // block table offset
+    int pad;
+};
+
+struct AttnShape {
+    int hq, hkv, hd;
+    int num_blocks;   // blocks per layer in the pool
+    int layer;        // layer index (selects the pool slice)
+    float scale_log2; // log2(e) / sqrt(hd)
+};
+
+cudaError_t prefill_attention(const CUtensorMap& tmap_q, const CUtensorMap& tmap_k,
+                              const CUtensorMap& tmap_v, const PrefillItem* items, int n_items,
+                              const int32_t* tables, __nv_bfloat16* out, const AttnShape& s,
+                              cudaStream_t stream);
+
+// Split-K paged decode attention. partial_* workspaces are sized by the caller for
+// n_items * hq * max_splits entries.
+cudaError_t decode_attention(const __nv_bfloat16* q, const __nv_bfloat16* k_pool,
+                             const __nv_bfloat16* v_pool, const DecodeItem* items, int n_items,
+                             int max_ctx, const int32_t* tables, __nv_bfloat16* out,
+                             float* part_o, float* part_ml, int max_splits, int num_sms,
+                             const AttnShape& s, cudaStream_t stream);
+
+int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits);
+
+}  // namespace asb

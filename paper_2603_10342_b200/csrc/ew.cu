@@ -1,0 +1,235 @@
+// HBM-bound elementwise / row kernels of the forward (K1 + K6 in SURVEY §2.3):
+//   weight init (counter-based splitmix64; bit-identical to oracle/forward.c),
+//   embedding gather, RMSNorm, RoPE + paged-KV append (the device half of
+//   KvCacheRegistry, /root/reference/proj/src/executor.cpp:166-205), greedy argmax.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "attn.h"
+#include "ew.h"
+#include "sm100.cuh"
+
+namespace asb {
+
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// element i of a named tensor: the (i+1)-th draw of Rng::substream(seed, name)
+// (/root/reference/proj/src/rng.hpp:28-37), mapped to a uniform bf16.
+__global__ void init_weights_kernel(__nv_bfloat16* dst, uint64_t state0, int64_t rows, int cols,
+                                    int row_mult, int row_off, int dst_cols, float offset,
+                                    float amp_scaled) {
+    const int64_t n = rows * cols;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t u = splitmix_mix(state0 + static_cast<uint64_t>(i + 1) * 0x9e3779b97f4a7c15ull);
+        const int32_t t = static_cast<int32_t>(u >> 40) - 8388608;
+        const float v = __fadd_rn(offset, __fmul_rn(static_cast<float>(t), amp_scaled));
+        const int64_t r = i / cols, c = i % cols;
+        dst[(r * row_mult + row_off) * dst_cols + c] = __float2bfloat16_rn(v);
+    }
+}
+
+__global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ emb,
+                             __nv_bfloat16* __restrict__ x, int T, int d) {
+    const int t = blockIdx.x;
+    if (t >= T) return;
+    const uint4* src = reinterpret_cast<const uint4*>(emb + static_cast<size_t>(ids[t]) * d);
+    uint4* dst = reinterpret_cast<uint4*>(x + static_cast<size_t>(t) * d);
+    for (int i = threadIdx.x; i < d / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+// One warp per row; y = bf16(x * (1/sqrt(mean(x^2)+eps)) * w).  rows_idx (optional)
+// gathers input rows (final norm of the logit rows only).
+__global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ rows_idx,
+                               const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y,
+                               int n_rows, int d, float eps) {
+    const int warps = blockDim.x >> 5;
+    const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= n_rows) return;
+    const int src_row = rows_idx ? rows_idx[row] : row;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(src_row) * d);
+    const uint4* wr = reinterpret_cast<const uint4*>(w);
+    uint4* yr = reinterpret_cast<uint4*>(y + static_cast<size_t>(row) * d);
+    const int nv = d / 8;
+    float ss = 0.f;
+    for (int i = lane; i < nv; i += 32) {
+        const uint4 v = xr[i];
+        const uint32_t a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float lo = bf16_lo(a[e]), hi = bf16_hi(a[e]);
+            ss += lo * lo + hi * hi;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, static_cast<float>(d)), eps)));
+    for (int i = lane; i < nv; i += 32) {
+        const uint4 v = xr[i], g = wr[i];
+        const uint32_t a[4] = {v.x, v.y, v.z, v.w};
+        const uint32_t b[4] = {g.x, g.y, g.z, g.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float lo = __fmul_rn(__fmul_rn(bf16_lo(a[e]), inv), bf16_lo(b[e]));
+            const float hi = __fmul_rn(__fmul_rn(bf16_hi(a[e]), inv), bf16_hi(b[e]));
+            o[e] = pack_bf16(lo, hi);
+        }
+        yr[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+// One CTA per token.  qkv row layout: [q heads | k heads | v heads] x hd.
+// q -> q_out (rotated), k -> K pool (rotated), v -> V pool at the token's slot.
+// Rotation: NeoX / Llama "rotate_half" with a host-built fp32 cos/sin table.
+__global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                   const int32_t* __restrict__ pos,
+                                   const int32_t* __restrict__ slot,
+                                   const float* __restrict__ cos_t, const float* __restrict__ sin_t,
+                                   __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_pool,
+                                   __nv_bfloat16* __restrict__ v_pool, int T, int hq, int hkv, int hd,
+                                   int layer, int num_blocks) {
+    const int t = blockIdx.x;
+    if (t >= T) return;
+    const int half = hd / 2;
+    const int p = pos[t];
+    const int sl = slot[t];
+    const int blk = sl / kBlockTokens, off = sl % kBlockTokens;
+    const __nv_bfloat16* row = qkv + static_cast<size_t>(t) * (hq + 2 * hkv) * hd;
+    const float* ct = cos_t + static_cast<size_t>(p) * half;
+    const float* st = sin_t + static_cast<size_t>(p) * half;
+    // rotated heads: q (hq) then k (hkv)
+    for (int i = threadIdx.x; i < (hq + hkv) * half; i += blockDim.x) {
+        const int h = i / half, j = i % half;
+        const float x1 = __bfloat162float(row[h * hd + j]);
+        const float x2 = __bfloat162float(row[h * hd + j + half]);
+        const float c = ct[j], s = st[j];
+        const float y1 = __fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, s));
+        const float y2 = __fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, s));
+        if (h < hq) {
+            __nv_bfloat16* qo = q_out + (static_cast<size_t>(t) * hq + h) * hd;
+            qo[j] = __float2bfloat16_rn(y1);
+            qo[j + half] = __float2bfloat16_rn(y2);
+        } else {
+            const int kh = h - hq;
+            __nv_bfloat16* kd =
+                k_pool + (((static_cast<size_t>(layer) * num_blocks + blk) * hkv + kh) * kBlockTokens + off) * hd;
+            kd[j] = __float2bfloat16_rn(y1);
+            kd[j + half] = __float2bfloat16_rn(y2);
+        }
+    }
+    for (int i = threadIdx.x; i < hkv * hd; i += blockDim.x) {
+        const int h = i / hd, j = i % hd;
+        __nv_bfloat16* vd =
+            v_pool + (((static_cast<size_t>(layer) * num_blocks + blk) * hkv + h) * kBlockTokens + off) * hd;
+        vd[j] = row[(hq + hkv + h) * hd + j];
+    }
+}
+
+// Greedy argmax per logits row (lowest index wins ties).  One CTA per row.
+__global__ void argmax_kernel(const float* __restrict__ logits, int V, int ld,
+                              int32_t* __restrict__ out_ids, float* __restrict__ out_max) {
+    const int row = blockIdx.x;
+    const float* lr = logits + static_cast<size_t>(row) * ld;
+    float best = -FLT_MAX;
+    int best_i = 0x7fffffff;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+        const float v = lr[i];
+        if (v > best) {  // strided scan in increasing i: first max is the lowest index
+            best = v;
+            best_i = i;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+        if (ob > best || (ob == best && oi < best_i)) {
+            best = ob;
+            best_i = oi;
+        }
+    }
+    __shared__ float sb[32];
+    __shared__ int si[32];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sb[w] = best;
+        si[w] = best_i;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        best = l < nw ? sb[l] : -FLT_MAX;
+        best_i = l < nw ? si[l] : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+            if (ob > best || (ob == best && oi < best_i)) {
+                best = ob;
+                best_i = oi;
+            }
+        }
+        if (l == 0) {
+            out_ids[row] = best_i;
+            if (out_max) out_max[row] = best;
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t init_weights(__nv_bfloat16* dst, uint64_t state0, int64_t rows, int cols, int row_mult,
+                         int row_off, float offset, float amp, cudaStream_t stream) {
+    const int64_t n = rows * cols;
+    int blocks = static_cast<int>((n + 255) / 256);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    init_weights_kernel<<<blocks, 256, 0, stream>>>(dst, state0, rows, cols, row_mult, row_off, cols,
+                                                    offset, amp * (1.0f / 8388608.0f));
+    return cudaGetLastError();
+}
+
+cudaError_t embed(const int32_t* ids, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int d,
+                  cudaStream_t stream) {
+    if (T <= 0) return cudaSuccess;
+    embed_kernel<<<T, 128, 0, stream>>>(ids, emb, x, T, d);
+    return cudaGetLastError();
+}
+
+cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows_idx, const __nv_bfloat16* w,
+                    __nv_bfloat16* y, int n_rows, int d, float eps, cudaStream_t stream) {
+    if (n_rows <= 0) return cudaSuccess;
+    const int warps = 8;
+    rmsnorm_kernel<<<(n_rows + warps - 1) / warps, warps * 32, 0, stream>>>(x, rows_idx, w, y, n_rows,
+                                                                          d, eps);
+    return cudaGetLastError();
+}
+
+cudaError_t rope_append(const __nv_bfloat16* qkv, const int32_t* pos, const int32_t* slot,
+                        const float* cos_t, const float* sin_t, __nv_bfloat16* q_out,
+                        __nv_bfloat16* k_pool, __nv_bfloat16* v_pool, int T, int hq, int hkv, int hd,
+                        int layer, int num_blocks, cudaStream_t stream) {
+    if (T <= 0) return cudaSuccess;
+    rope_append_kernel<<<T, 256, 0, stream>>>(qkv, pos, slot, cos_t, sin_t, q_out, k_pool, v_pool, T,
+                                             hq, hkv, hd, layer, num_blocks);
+    return cudaGetLastError();
+}
+
+cudaError_t argmax_rows(const float* logits, int rows, int V, int ld, int32_t* out_ids,
+                        float* out_max, cudaStream_t stream) {
+    if (rows <= 0) return cudaSuccess;
+    argmax_kernel<<<rows, 1024, 0, stream>>>(logits, V, ld, out_ids, out_max);
+    return cudaGetLastError();
+}
+
+}  // namespace asb

@@ -1,0 +1,912 @@
+// Device runtime behind the asb_* C ABI (include/agentserve_b200.h): model weights,
+// paged KV pool + host block allocator (with the reference KvCacheRegistry protocol),
+// execution lanes and the ragged-batch SLM forward.
+//
+// The forward is the work the reference simulates at its two seams:
+//   decode step  -> decode_step_duration_ms   (/root/reference/proj/src/executor.cpp:207-220)
+//   prefill unit -> remaining / rate           (/root/reference/proj/src/engine.cpp:450-475)
+// Numerics contract (restated by oracle/forward.c): bf16 storage of x / h / qkv / q / k / v /
+// attn / act, fp32 accumulation, single rounding after bias / residual / SiLU·mul epilogues.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/agentserve_b200.h"
+#include "attn.h"
+#include "ew.h"
+#include "gemm.h"
+#include "json.hpp"
+#include "runtime.h"
+
+using asb::kBlockTokens;
+using nlohmann::json;
+
+namespace asb {
+
+thread_local std::string g_err;
+
+struct AsbError : std::runtime_error {
+    asb_status st;
+    AsbError(asb_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+[[noreturn]] void fail(asb_status s, const std::string& m) { throw AsbError(s, m); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        fail(ASB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+template <typename Fn>
+asb_status guarded(Fn&& fn) {
+    try {
+        fn();
+        return ASB_OK;
+    } catch (const AsbError& e) {
+        g_err = e.what();
+        return e.st;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return ASB_ERR_INVALID_ARGUMENT;
+    }
+}
+
+// ------------------------------------------------------------------ model spec
+static uint64_t fnv1a(const std::string& s) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (unsigned char c : s) {
+        h ^= c;
+        h *= 0x00000100000001b3ull;
+    }
+    return h;
+}
+static uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+uint64_t substream_state(uint64_t seed, const std::string& name) { return mix64(seed ^ fnv1a(name)); }
+
+ModelSpec spec_preset(const std::string& name) {
+    ModelSpec s;
+    s.name = name;
+    if (name == "tiny") {
+        s.layers = 2; s.d = 256; s.hq = 4; s.hkv = 2; s.hd = 64; s.ffn = 704; s.vocab = 4096;
+        s.tied = true; s.qkv_bias = false; s.theta = 10000.0; s.eps = 1e-6f;
+    } else if (name == "qwen2.5-0.5b") {
+        s.layers = 24; s.d = 896; s.hq = 14; s.hkv = 2; s.hd = 64; s.ffn = 4864; s.vocab = 151936;
+        s.tied = true; s.qkv_bias = true; s.theta = 1000000.0; s.eps = 1e-6f;
+    } else if (name == "llama3.2-3b") {
+        s.layers = 28; s.d = 3072; s.hq = 24; s.hkv = 8; s.hd = 128; s.ffn = 8192; s.vocab = 128256;
+        s.tied = true; s.qkv_bias = false; s.theta = 500000.0; s.eps = 1e-5f;
+        s.rope_llama3 = true; s.rope_factor = 32.0; s.rope_lo = 1.0; s.rope_hi = 4.0; s.rope_orig = 8192;
+    } else if (name == "qwen2.5-7b") {
+        s.layers = 28; s.d = 3584; s.hq = 28; s.hkv = 4; s.hd = 128; s.ffn = 18944; s.vocab = 152064;
+        s.tied = false; s.qkv_bias = true; s.theta = 1000000.0; s.eps = 1e-6f;
+    } else if (name == "llama3.1-8b") {
+        s.layers = 32; s.d = 4096; s.hq = 32; s.hkv = 8; s.hd = 128; s.ffn = 14336; s.vocab = 128256;
+        s.tied = false; s.qkv_bias = false; s.theta = 500000.0; s.eps = 1e-5f;
+        s.rope_llama3 = true; s.rope_factor = 8.0; s.rope_lo = 1.0; s.rope_hi = 4.0; s.rope_orig = 8192;
+    } else {
+        fail(ASB_ERR_VALIDATION, "unknown model preset '" + name + "'");
+    }
+    return s;
+}
+
+ModelSpec parse_spec(const std::string& text) {
+    if (text.empty() || text[0] != '{') return spec_preset(text);
+    json j;
+    try {
+        j = json::parse(text);
+    } catch (const json::exception& e) {
+        fail(ASB_ERR_VALIDATION, std::string("model spec is not JSON: ") + e.what());
+    }
+    ModelSpec s = j.contains("preset") ? spec_preset(j["preset"].get<std::string>()) : ModelSpec{};
+    if (!j.contains("preset")) s.name = j.value("name", std::string("custom"));
+    s.layers = j.value("layers", s.layers);
+    s.d = j.value("d_model", s.d);
+    s.hq = j.value("n_heads", s.hq);
+    s.hkv = j.value("n_kv_heads", s.hkv);
+    s.hd = j.value("head_dim", s.hd);
+    s.ffn = j.value("ffn", s.ffn);
+    s.vocab = j.value("vocab", s.vocab);
+    s.tied = j.value("tied", s.tied);
+    s.qkv_bias = j.value("qkv_bias", s.qkv_bias);
+    s.theta = j.value("rope_theta", s.theta);
+    s.eps = j.value("rms_eps", s.eps);
+    return s;
+}
+
+void validate_spec(const ModelSpec& s) {
+    if (s.layers < 1 || s.d < 64 || s.hq < 1 || s.hkv < 1 || s.vocab < 2 || s.ffn < 64)
+        fail(ASB_ERR_VALIDATION, "model spec: non-positive dimension");
+    if (s.hd != 64 && s.hd != 128) fail(ASB_ERR_VALIDATION, "model spec: head_dim must be 64 or 128");
+    if (s.hq % s.hkv != 0 || s.hq / s.hkv > 8)
+        fail(ASB_ERR_VALIDATION, "model spec: n_heads must be a multiple of n_kv_heads, group <= 8");
+    if (s.d % 64 || s.ffn % 64 || (s.hq * s.hd) % 64)
+        fail(ASB_ERR_VALIDATION, "model spec: d_model, ffn and n_heads*head_dim must be multiples of 64");
+}
+
+// RoPE inverse frequencies (double), Llama-3 wavelength scaling when requested.
+std::vector<double> rope_inv_freq(const ModelSpec& s) {
+    const int half = s.hd / 2;
+    std::vector<double> f(half);
+    for (int i = 0; i < half; ++i) {
+        double inv = 1.0 / std::pow(s.theta, (2.0 * i) / s.hd);
+        if (s.rope_llama3) {
+            const double lo_wl = s.rope_orig / s.rope_lo, hi_wl = s.rope_orig / s.rope_hi;
+            const double wl = 2.0 * M_PI / inv;
+            if (wl > lo_wl) {
+                inv = inv / s.rope_factor;
+            } else if (wl >= hi_wl) {
+                const double smooth = (s.rope_orig / wl - s.rope_lo) / (s.rope_hi - s.rope_lo);
+                inv = (1.0 - smooth) * inv / s.rope_factor + smooth * inv;
+            }
+        }
+        f[i] = inv;
+    }
+    return f;
+}
+
+// ------------------------------------------------------------------ weights
+static void* dmalloc(size_t bytes, std::vector<void*>& track) {
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+    track.push_back(p);
+    return p;
+}
+
+static void weight_maps(Weight& w) {
+    if (!make_tmap_bf16(&w.map_b256, w.ptr, w.rows, w.cols, w.cols, 256) ||
+        !make_tmap_bf16(&w.map_a128, w.ptr, w.rows, w.cols, w.cols, 128))
+        fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for a weight");
+}
+
+}  // namespace asb
+
+using namespace asb;
+
+// =================================================================== model
+struct asb_model {
+    ModelSpec spec;
+    int device = 0;
+    int num_sms = 148;
+    uint64_t seed = 0;
+    int max_ctx = 0;
+    std::vector<void*> allocs;
+    Weight embed, lm_head;
+    __nv_bfloat16* final_norm = nullptr;
+    struct Layer {
+        __nv_bfloat16 *attn_norm, *mlp_norm, *qkv_bias;
+        Weight qkv, o, gate_up, down;
+    };
+    std::vector<Layer> layers;
+    float *cos_t = nullptr, *sin_t = nullptr;
+
+    ~asb_model() {
+        cudaSetDevice(device);
+        for (void* p : allocs) cudaFree(p);
+    }
+};
+
+namespace {
+
+void fill(const asb_model* m, __nv_bfloat16* dst, const std::string& name, int64_t rows, int cols,
+          int row_mult, int row_off, float offset, float amp) {
+    cuda_check(init_weights(dst, substream_state(m->seed, name), rows, cols, row_mult, row_off, offset,
+                            amp, nullptr),
+               "init_weights");
+}
+
+constexpr float kAmpW = 0.034641016f;  // uniform amplitude with std 0.02
+constexpr float kAmpB = 0.1f;
+constexpr float kAmpN = 0.1f;
+
+}  // namespace
+
+// =================================================================== kv
+struct asb_kv {
+    asb_model* m = nullptr;
+    int nb = 0;
+    __nv_bfloat16 *k_pool = nullptr, *v_pool = nullptr;
+    CUtensorMap tk, tv;
+    std::vector<int> free_list;  // LIFO: back() is handed out next
+    struct Sess {
+        std::vector<int32_t> blocks;
+        int len = 0;
+        int prefix = 0;
+        bool sealed = false;
+    };
+    std::map<uint32_t, Sess> sess;
+
+    ~asb_kv() {
+        cudaSetDevice(m->device);
+        cudaFree(k_pool);
+        cudaFree(v_pool);
+    }
+    Sess& get(uint32_t s) { return sess[s]; }
+    void ensure(Sess& s, int new_len) {
+        const int need = (new_len + kBlockTokens - 1) / kBlockTokens;
+        while (static_cast<int>(s.blocks.size()) < need) {
+            if (free_list.empty())
+                fail(ASB_ERR_INFEASIBLE, "KV pool exhausted (" + std::to_string(nb) + " blocks)");
+            s.blocks.push_back(free_list.back());
+            free_list.pop_back();
+        }
+    }
+};
+
+// =================================================================== lane
+struct asb_lane {
+    asb_model* m = nullptr;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int max_T = 0, max_segs = 0, max_tbl = 0, max_pitems = 0, max_splits = 16;
+    __nv_bfloat16 *x, *h, *qkv, *q, *attn, *act, *hl;
+    float *logits, *ws, *part_o, *part_ml;
+    int32_t* d_meta = nullptr;
+    int32_t* h_meta = nullptr;
+    int32_t* d_out = nullptr;
+    int32_t* h_out = nullptr;
+    size_t meta_ints = 0;
+    std::vector<void*> allocs;
+    // tensor maps of GEMM inputs: [0] box 128 (normal A), [1..4] box 32/64/128/256 (swap B)
+    CUtensorMap map_h[5], map_attn[5], map_act[5], map_hl[5], map_q;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool launched = false;
+    int last_logit_rows = 0;
+
+    ~asb_lane() {
+        cudaSetDevice(m->device);
+        if (launched) cudaStreamSynchronize(stream);
+        for (void* p : allocs) cudaFree(p);
+        if (h_meta) cudaFreeHost(h_meta);
+        if (h_out) cudaFreeHost(h_out);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (own_stream && stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+void act_maps(CUtensorMap* maps, const void* base, int rows, int cols) {
+    const int boxes[5] = {128, 32, 64, 128, 256};
+    for (int i = 0; i < 5; ++i)
+        if (!make_tmap_bf16(&maps[i], base, rows, cols, cols, boxes[i]))
+            fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for an activation");
+}
+
+int swap_map_index(int bn) { return bn == 32 ? 1 : bn == 64 ? 2 : bn == 128 ? 3 : 4; }
+
+// Y[T][n_out] = X[T][k] . W^T with the path chosen by T.
+void linear(asb_lane* L, const CUtensorMap* xmaps, const Weight& w, int T, int epi,
+            __nv_bfloat16* out, int ldo, const __nv_bfloat16* bias, const __nv_bfloat16* resid,
+            float* out_f32, int force_path = -1, int force_splits = 0) {
+    GemmParams p{};
+    p.tokens = T;
+    p.n_out = w.rows;
+    p.K = w.cols;
+    p.epi = epi;
+    p.out = out;
+    p.out_f32 = out_f32;
+    p.ldo = ldo;
+    p.bias = bias;
+    p.resid = resid;
+    p.ldr = ldo;
+    p.ws = L->ws;
+    const int num_sms = L->m->num_sms;
+    const bool swap = force_path >= 0 ? force_path == 1 : T <= 256;
+    cudaError_t e;
+    if (swap) {
+        const int bn = gemm_pick_bn(T);
+        p.swap = 1;
+        p.M = w.rows;
+        p.N = T;
+        const int tiles = (w.rows + 127) / 128;
+        const int kb = (w.cols + 63) / 64;
+        int splits = force_splits > 0 ? force_splits : (num_sms + tiles - 1) / tiles;
+        if (force_splits <= 0) splits = std::min(splits, std::max(1, kb / 4));
+        if (epi == EPI_F32 && force_splits <= 0) splits = 1;
+        p.splits = splits;
+        e = gemm_launch(w.map_a128, xmaps[swap_map_index(bn)], p, bn, num_sms, L->stream);
+    } else {
+        p.swap = 0;
+        p.M = T;
+        p.N = w.rows;
+        const int tm = (T + 127) / 128;
+        const int t256 = tm * ((w.rows + 255) / 256);
+        const int bn = (t256 < (num_sms * 4) / 5) ? 128 : 256;
+        p.splits = 1;
+        // normal path: B = W.  bn==128 reuses the box-128 weight map.
+        e = gemm_launch(xmaps[0], bn == 256 ? w.map_b256 : w.map_a128, p, bn, num_sms, L->stream);
+    }
+    cuda_check(e, "gemm launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* asb_last_error(void) { return g_err.c_str(); }
+
+const char* asb_status_name(asb_status s) {
+    switch (s) {
+    case ASB_OK: return "ok";
+    case ASB_ERR_INVALID_ARGUMENT: return "invalid_argument";
+    case ASB_ERR_VALIDATION: return "validation_error";
+    case ASB_ERR_PROTOCOL: return "protocol_error";
+    case ASB_ERR_IO: return "io_error";
+    case ASB_ERR_NO_DATA: return "no_data";
+    case ASB_ERR_INFEASIBLE: return "infeasible";
+    case ASB_ERR_CUDA: return "cuda_error";
+    }
+    return "unknown";
+}
+
+void asb_string_free(char* s) { delete[] s; }
+
+const char* asb_build_info(void) { return "sm_100a;agentserve_b200 r1"; }
+
+asb_status asb_model_create(const char* model, uint64_t seed, int device, int max_context,
+                            asb_model** out) {
+    if (!model || !out) {
+        g_err = "null argument";
+        return ASB_ERR_INVALID_ARGUMENT;
+    }
+    return guarded([&] {
+        ModelSpec s = parse_spec(model);
+        validate_spec(s);
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device)
+            fail(ASB_ERR_CUDA, "no CUDA device " + std::to_string(device));
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10)
+            fail(ASB_ERR_CUDA, std::string("device is not sm_100 (") + prop.name + ")");
+        auto m = std::make_unique<asb_model>();
+        m->spec = s;
+        m->device = device;
+        m->num_sms = prop.multiProcessorCount;
+        m->seed = seed;
+        m->max_ctx = max_context > 0 ? max_context : 16384;
+        auto mk = [&](int rows, int cols) {
+            Weight w;
+            w.rows = rows;
+            w.cols = cols;
+            w.ptr = static_cast<__nv_bfloat16*>(dmalloc(size_t(rows) * cols * 2, m->allocs));
+            return w;
+        };
+        auto vec = [&](int n) {
+            return static_cast<__nv_bfloat16*>(dmalloc(size_t(n) * 2, m->allocs));
+        };
+        const int qd = s.hq * s.hd, kvd = s.hkv * s.hd;
+        m->embed = mk(s.vocab, s.d);
+        fill(m.get(), m->embed.ptr, "embed", s.vocab, s.d, 1, 0, 0.f, kAmpW);
+        weight_maps(m->embed);
+        if (s.tied) {
+            m->lm_head = m->embed;
+        } else {
+            m->lm_head = mk(s.vocab, s.d);
+            fill(m.get(), m->lm_head.ptr, "lm_head", s.vocab, s.d, 1, 0, 0.f, kAmpW);
+            weight_maps(m->lm_head);
+        }
+        m->final_norm = vec(s.d);
+        fill(m.get(), m->final_norm, "final_norm", 1, s.d, 1, 0, 1.f, kAmpN);
+        for (int l = 0; l < s.layers; ++l) {
+            asb_model::Layer ly{};
+            const std::string p = "L" + std::to_string(l) + "/";
+            ly.attn_norm = vec(s.d);
+            fill(m.get(), ly.attn_norm, p + "attn_norm", 1, s.d, 1, 0, 1.f, kAmpN);
+            ly.mlp_norm = vec(s.d);
+            fill(m.get(), ly.mlp_norm, p + "mlp_norm", 1, s.d, 1, 0, 1.f, kAmpN);
+            ly.qkv = mk(qd + 2 * kvd, s.d);
+            fill(m.get(), ly.qkv.ptr, p + "q", qd, s.d, 1, 0, 0.f, kAmpW);
+            fill(m.get(), ly.qkv.ptr + size_t(qd) * s.d, p + "k", kvd, s.d, 1, 0, 0.f, kAmpW);
+            fill(m.get(), ly.qkv.ptr + size_t(qd + kvd) * s.d, p + "v", kvd, s.d, 1, 0, 0.f, kAmpW);
+            weight_maps(ly.qkv);
+            ly.qkv_bias = nullptr;
+            if (s.qkv_bias) {
+                ly.qkv_bias = vec(qd + 2 * kvd);
+                fill(m.get(), ly.qkv_bias, p + "q_bias", 1, qd, 1, 0, 0.f, kAmpB);
+                fill(m.get(), ly.qkv_bias + qd, p + "k_bias", 1, kvd, 1, 0, 0.f, kAmpB);
+                fill(m.get(), ly.qkv_bias + qd + kvd, p + "v_bias", 1, kvd, 1, 0, 0.f, kAmpB);
+            }
+            ly.o = mk(s.d, qd);
+            fill(m.get(), ly.o.ptr, p + "o", s.d, qd, 1, 0, 0.f, kAmpW);
+            weight_maps(ly.o);
+            // gate/up interleaved: row 2j = gate_j, row 2j+1 = up_j (SiLU·mul epilogue pairs)
+            ly.gate_up = mk(2 * s.ffn, s.d);
+            fill(m.get(), ly.gate_up.ptr, p + "gate", s.ffn, s.d, 2, 0, 0.f, kAmpW);
+            fill(m.get(), ly.gate_up.ptr, p + "up", s.ffn, s.d, 2, 1, 0.f, kAmpW);
+            weight_maps(ly.gate_up);
+            ly.down = mk(s.d, s.ffn);
+            fill(m.get(), ly.down.ptr, p + "down", s.d, s.ffn, 1, 0, 0.f, kAmpW);
+            weight_maps(ly.down);
+            m->layers.push_back(ly);
+        }
+        // RoPE tables
+        const int half = s.hd / 2;
+        std::vector<double> inv = rope_inv_freq(s);
+        std::vector<float> c(size_t(m->max_ctx) * half), sn(size_t(m->max_ctx) * half);
+        for (int pos = 0; pos < m->max_ctx; ++pos)
+            for (int i = 0; i < half; ++i) {
+                const double a = pos * inv[i];
+                c[size_t(pos) * half + i] = static_cast<float>(std::cos(a));
+                sn[size_t(pos) * half + i] = static_cast<float>(std::sin(a));
+            }
+        m->cos_t = static_cast<float*>(dmalloc(c.size() * 4, m->allocs));
+        m->sin_t = static_cast<float*>(dmalloc(sn.size() * 4, m->allocs));
+        cuda_check(cudaMemcpy(m->cos_t, c.data(), c.size() * 4, cudaMemcpyHostToDevice), "copy rope");
+        cuda_check(cudaMemcpy(m->sin_t, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice), "copy rope");
+        cuda_check(cudaDeviceSynchronize(), "weight init");
+        *out = m.release();
+    });
+}
+
+asb_status asb_model_describe(const asb_model* m, char** out_json) {
+    if (!m || !out_json) {
+        g_err = "null argument";
+        return ASB_ERR_INVALID_ARGUMENT;
+    }
+    return guarded([&] {
+        const ModelSpec& s = m->spec;
+        json j = {{"name", s.name},       {"layers", s.layers},     {"d_model", s.d},
+                  {"n_heads", s.hq},      {"n_kv_heads", s.hkv},    {"head_dim", s.hd},
+                  {"ffn", s.ffn},         {"vocab", s.vocab},       {"tied", s.tied},
+                  {"qkv_bias", s.qkv_bias}, {"rope_theta", s.theta}, {"rms_eps", s.eps},
+                  {"rope_llama3", s.rope_llama3}, {"rope_factor", s.rope_factor},
+                  {"rope_lo", s.rope_lo}, {"rope_hi", s.rope_hi}, {"rope_orig", s.rope_orig},
+                  {"seed", m->seed},      {"num_sms", m->num_sms},  {"max_context", m->max_ctx},
+                  {"block_tokens", kBlockTokens}};
+        const std::string t = j.dump();
+        char* o = new char[t.size() + 1];
+        std::memcpy(o, t.c_str(), t.size() + 1);
+        *out_json = o;
+    });
+}
+
+void asb_model_free(asb_model* m) { delete m; }
+
+int asb_kv_block_tokens(void) { return kBlockTokens; }
+
+asb_status asb_kv_create(asb_model* m, int num_blocks, asb_kv** out) {
+    if (!m || !out || num_blocks < 1) {
+        g_err = "invalid argument";
+        return ASB_ERR_INVALID_ARGUMENT;
+    }
+    return guarded([&] {
+        cuda_check(cudaSetDevice(m->device), "cudaSetDevice");
+        auto kv = std::make_unique<asb_kv>();
+        kv->m = m;
+        kv->nb = num_blocks;
+        const ModelSpec& s = m->spec;
+        const size_t elems = size_t(s.layers) * num_blocks * s.hkv * kBlockTokens * s.hd;
+        cuda_check(cudaMalloc(&kv->k_pool, elems * 2), "cudaMalloc K pool");
+        cuda_check(cudaMalloc(&kv->v_pool, elems * 2), "cudaMalloc V pool");
+        // zero so masked tail rows of a block are finite (0 * garbage must not be NaN)
+        cuda_check(cudaMemset(kv->k_pool, 0, elems * 2), "memset");
+        cuda_check(cudaMemset(kv->v_pool, 0, elems * 2), "memset");
+        const long rows = long(s.layers) * num_blocks * s.hkv * kBlockTokens;
+        if (rows >= (1l << 31)) fail(ASB_ERR_VALIDATION, "KV pool too large for 32-bit TMA rows");
+        if (!make_tmap_bf16(&kv->tk, kv->k_pool, int(rows), s.hd, s.hd, kBlockTokens) ||
+            !make_tmap_bf16(&kv->tv, kv->v_pool, int(rows), s.hd, s.hd, kBlockTokens))
+            fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for the KV pool");
+        kv->free_list.reserve(num_blocks);
+        for (int b = num_blocks - 1; b >= 0; --b) kv->free_list.push_back(b);
+        cuda_check(cudaDeviceSynchronize(), "kv init");
+        *out = kv.release();
+    });
+}
+
+void asb_kv_free(asb_kv* kv) { delete kv; }
+
+int asb_kv_free_blocks(const asb_kv* kv) { return kv ? int(kv->free_list.size()) : -1; }
+
+asb_status asb_kv_begin_write(asb_kv* kv, uint32_t session) {
+    if (!kv) return ASB_ERR_INVALID_ARGUMENT;
+    kv->get(session).sealed = false;
+    return ASB_OK;
+}
+
+asb_status asb_kv_commit(asb_kv* kv, uint32_t session, int new_prefix) {
+    if (!kv) return ASB_ERR_INVALID_ARGUMENT;
+    return guarded([&] {
+        auto& s = kv->get(session);
+        if (new_prefix < s.prefix)
+            fail(ASB_ERR_PROTOCOL, "kv commit shrinks session " + std::to_string(session) +
+                                       " prefix from " + std::to_string(s.prefix) + " to " +
+                                       std::to_string(new_prefix));
+        s.prefix = new_prefix;
+        s.sealed = true;
+    });
+}
+
+asb_status asb_kv_append(asb_kv* kv, uint32_t session, int tokens) {
+    if (!kv) return ASB_ERR_INVALID_ARGUMENT;
+    return guarded([&] {
+        auto& s = kv->get(session);
+        if (!s.sealed)
+            fail(ASB_ERR_PROTOCOL, "decode append on unsealed KV entry for session " +
+                                       std::to_string(session));
+        s.prefix += tokens;
+    });
+}
+
+int asb_kv_sealed(const asb_kv* kv, uint32_t session) {
+    if (!kv) return 0;
+    auto it = kv->sess.find(session);
+    return it != kv->sess.end() && it->second.sealed ? 1 : 0;
+}
+
+asb_status asb_kv_require_sealed(const asb_kv* kv, uint32_t session) {
+    if (!kv) return ASB_ERR_INVALID_ARGUMENT;
+    if (!asb_kv_sealed(kv, session)) {
+        g_err = "decode step on unsealed KV entry for session " + std::to_string(session);
+        return ASB_ERR_PROTOCOL;
+    }
+    return ASB_OK;
+}
+
+int asb_kv_prefix(const asb_kv* kv, uint32_t session) {
+    if (!kv) return -1;
+    auto it = kv->sess.find(session);
+    return it == kv->sess.end() ? 0 : it->second.prefix;
+}
+
+int asb_kv_length(const asb_kv* kv, uint32_t session) {
+    if (!kv) return -1;
+    auto it = kv->sess.find(session);
+    return it == kv->sess.end() ? 0 : it->second.len;
+}
+
+asb_status asb_kv_block_table(const asb_kv* kv, uint32_t session, int32_t* out, int cap, int* n) {
+    if (!kv || !n) return ASB_ERR_INVALID_ARGUMENT;
+    auto it = kv->sess.find(session);
+    const int cnt = it == kv->sess.end() ? 0 : int(it->second.blocks.size());
+    *n = cnt;
+    if (out)
+        for (int i = 0; i < std::min(cap, cnt); ++i) out[i] = it->second.blocks[i];
+    return ASB_OK;
+}
+
+asb_status asb_kv_release(asb_kv* kv, uint32_t session) {
+    if (!kv) return ASB_ERR_INVALID_ARGUMENT;
+    auto it = kv->sess.find(session);
+    if (it == kv->sess.end()) return ASB_OK;
+    // return blocks in reverse so a re-allocation hands them out in the same order
+    for (auto b = it->second.blocks.rbegin(); b != it->second.blocks.rend(); ++b)
+        kv->free_list.push_back(*b);
+    kv->sess.erase(it);
+    return ASB_OK;
+}
+
+asb_status asb_kv_read_token(const asb_kv* kv, uint32_t session, int position, uint16_t* k_out,
+                             uint16_t* v_out) {
+    if (!kv || !k_out || !v_out) return ASB_ERR_INVALID_ARGUMENT;
+    return guarded([&] {
+        auto it = kv->sess.find(session);
+        if (it == kv->sess.end() || position < 0 || position >= it->second.len)
+            fail(ASB_ERR_INVALID_ARGUMENT, "position not written for session");
+        const ModelSpec& s = kv->m->spec;
+        const int blk = it->second.blocks[position / kBlockTokens];
+        const int off = position % kBlockTokens;
+        cuda_check(cudaSetDevice(kv->m->device), "cudaSetDevice");
+        for (int l = 0; l < s.layers; ++l)
+            for (int h = 0; h < s.hkv; ++h) {
+                const size_t src =
+                    (((size_t(l) * kv->nb + blk) * s.hkv + h) * kBlockTokens + off) * s.hd;
+                const size_t dst = (size_t(l) * s.hkv + h) * s.hd;
+                cuda_check(cudaMemcpy(k_out + dst, kv->k_pool + src, s.hd * 2, cudaMemcpyDeviceToHost), "copy");
+                cuda_check(cudaMemcpy(v_out + dst, kv->v_pool + src, s.hd * 2, cudaMemcpyDeviceToHost), "copy");
+            }
+    });
+}
+
+asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void* stream,
+                           asb_lane** out) {
+    if (!m || !out || max_tokens < 1 || max_segments < 1) {
+        g_err = "invalid argument";
+        return ASB_ERR_INVALID_ARGUMENT;
+    }
+    return guarded([&] {
+        cuda_check(cudaSetDevice(m->device), "cudaSetDevice");
+        auto L = std::make_unique<asb_lane>();
+        L->m = m;
+        const ModelSpec& s = m->spec;
+        L->max_T = max_tokens;
+        L->max_segs = std::min(max_segments, max_tokens);
+        L->max_tbl = L->max_segs * ((m->max_ctx + kBlockTokens - 1) / kBlockTokens);
+        L->max_pitems = max_tokens / 128 + L->max_segs;
+        if (stream) {
+            L->stream = static_cast<cudaStream_t>(stream);
+        } else {
+            cuda_check(cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking), "stream");
+            L->own_stream = true;
+        }
+        const int T = max_tokens;
+        const int qd = s.hq * s.hd, kvd = s.hkv * s.hd;
+        auto bf = [&](size_t n) { return static_cast<__nv_bfloat16*>(dmalloc(n * 2, L->allocs)); };
+        L->x = bf(size_t(T) * s.d);
+        L->h = bf(size_t(T) * s.d);
+        L->qkv = bf(size_t(T) * (qd + 2 * kvd));
+        L->q = bf(size_t(T) * qd);
+        L->attn = bf(size_t(T) * qd);
+        L->act = bf(size_t(T) * s.ffn);
+        L->hl = bf(size_t(L->max_segs) * s.d);
+        L->logits = static_cast<float*>(dmalloc(size_t(L->max_segs) * s.vocab * 4, L->allocs));
+        const int ws_rows = std::min(T, 256);
+        const size_t ws_cols = std::max<size_t>({size_t(2) * s.ffn, size_t(qd + 2 * kvd), size_t(s.d)});
+        L->ws = static_cast<float*>(dmalloc(size_t(ws_rows) * ws_cols * 4, L->allocs));
+        cuda_check(cudaMemset(L->ws, 0, size_t(ws_rows) * ws_cols * 4), "memset ws");
+        const int dec_rows = std::min(L->max_segs, T);
+        L->part_o = static_cast<float*>(
+            dmalloc(size_t(dec_rows) * s.hq * L->max_splits * s.hd * 4, L->allocs));
+        L->part_ml = static_cast<float*>(
+            dmalloc(size_t(dec_rows) * s.hq * L->max_splits * 2 * 4, L->allocs));
+        L->meta_ints = size_t(3) * T + L->max_segs + L->max_tbl + 4 * size_t(L->max_segs) +
+                       4 * size_t(L->max_pitems) + 64;
+        L->d_meta = static_cast<int32_t*>(dmalloc(L->meta_ints * 4, L->allocs));
+        cuda_check(cudaMallocHost(&L->h_meta, L->meta_ints * 4), "cudaMallocHost");
+        L->d_out = static_cast<int32_t*>(dmalloc(size_t(L->max_segs) * 4, L->allocs));
+        cuda_check(cudaMallocHost(&L->h_out, size_t(L->max_segs) * 4), "cudaMallocHost");
+        act_maps(L->map_h, L->h, T, s.d);
+        act_maps(L->map_attn, L->attn, T, qd);
+        act_maps(L->map_act, L->act, T, s.ffn);
+        act_maps(L->map_hl, L->hl, L->max_segs, s.d);
+        if (!make_tmap_bf16(&L->map_q, L->q, T, qd, qd, 128))
+            fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for q");
+        cuda_check(cudaEventCreate(&L->ev0), "event");
+        cuda_check(cudaEventCreate(&L->ev1), "event");
+        cuda_check(cudaDeviceSynchronize(), "lane init");
+        *out = L.release();
+    });
+}
+
+void asb_lane_free(asb_lane* lane) { delete lane; }
+
+asb_status asb_lane_set_stream(asb_lane* lane, void* stream) {
+    if (!lane || !stream) return ASB_ERR_INVALID_ARGUMENT;
+    if (lane->launched) cudaStreamSynchronize(lane->stream);
+    if (lane->own_stream) cudaStreamDestroy(lane->stream);
+    lane->own_stream = false;
+    lane->stream = static_cast<cudaStream_t>(stream);
+    return ASB_OK;
+}
+
+void* asb_lane_stream(const asb_lane* lane) { return lane ? lane->stream : nullptr; }
+
+int asb_lane_query(const asb_lane* lane) {
+    if (!lane || !lane->launched) return 1;
+    return cudaEventQuery(lane->ev1) == cudaSuccess ? 1 : 0;
+}
+
+asb_status asb_lane_wait(asb_lane* lane) {
+    if (!lane) return ASB_ERR_INVALID_ARGUMENT;
+    if (!lane->launched) return ASB_OK;
+    return guarded([&] { cuda_check(cudaEventSynchronize(lane->ev1), "lane wait"); });
+}
+
+float asb_lane_last_ms(const asb_lane* lane) {
+    if (!lane || !lane->launched) return -1.f;
+    float ms = -1.f;
+    if (cudaEventElapsedTime(&ms, lane->ev0, lane->ev1) != cudaSuccess) return -1.f;
+    return ms;
+}
+
+asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_segs,
+                       const int32_t* tokens) {
+    if (!L || !kv || !segs || !tokens || n_segs < 1) {
+        g_err = "invalid argument";
+        return ASB_ERR_INVALID_ARGUMENT;
+    }
+    return guarded([&] {
+        asb_model* m = L->m;
+        const ModelSpec& s = m->spec;
+        if (kv->m != m) fail(ASB_ERR_INVALID_ARGUMENT, "kv belongs to another model");
+        if (n_segs > L->max_segs) fail(ASB_ERR_INVALID_ARGUMENT, "too many segments for lane");
+        int T = 0;
+        for (int i = 0; i < n_segs; ++i) {
+            if (segs[i].n_tokens < 1) fail(ASB_ERR_INVALID_ARGUMENT, "segment with no tokens");
+            T += segs[i].n_tokens;
+        }
+        if (T > L->max_T) fail(ASB_ERR_INVALID_ARGUMENT, "batch exceeds lane max_tokens");
+        cuda_check(cudaSetDevice(m->device), "cudaSetDevice");
+        // previous launch must be done before the pinned staging is reused
+        if (L->launched) cuda_check(cudaEventSynchronize(L->ev1), "lane reuse");
+
+        // ---- host metadata ------------------------------------------------------------
+        int32_t* hm = L->h_meta;
+        int32_t* h_tok = hm;
+        int32_t* h_pos = h_tok + T;
+        int32_t* h_slot = h_pos + T;
+        int32_t* h_lrows = h_slot + T;
+        int n_logit = 0;
+        std::vector<int32_t> tbl;
+        std::vector<DecodeItem> ditems;
+        std::vector<PrefillItem> pitems;
+        int max_ctx = 0;
+        int row = 0;
+        for (int i = 0; i < n_segs; ++i) {
+            const asb_segment& g = segs[i];
+            auto& ss = kv->get(g.session);
+            const int start = ss.len;
+            if (start + g.n_tokens > m->max_ctx)
+                fail(ASB_ERR_INFEASIBLE, "session " + std::to_string(g.session) +
+                                              " exceeds max_context");
+            kv->ensure(ss, start + g.n_tokens);
+            const int toff = int(tbl.size());
+            tbl.insert(tbl.end(), ss.blocks.begin(), ss.blocks.end());
+            for (int t = 0; t < g.n_tokens; ++t) {
+                const int p = start + t;
+                h_tok[row + t] = tokens[row + t];
+                h_pos[row + t] = p;
+                h_slot[row + t] = ss.blocks[p / kBlockTokens] * kBlockTokens + p % kBlockTokens;
+            }
+            if (g.n_tokens == 1) {
+                ditems.push_back(DecodeItem{row, start + 1, toff, 0});
+                max_ctx = std::max(max_ctx, start + 1);
+            } else {
+                for (int q0 = 0; q0 < g.n_tokens; q0 += 128)
+                    pitems.push_back(PrefillItem{row + q0, start + q0, std::min(128, g.n_tokens - q0), toff});
+            }
+            if (g.want_logits) h_lrows[n_logit++] = row + g.n_tokens - 1;
+            ss.len = start + g.n_tokens;
+            row += g.n_tokens;
+        }
+        if (int(tbl.size()) > L->max_tbl) fail(ASB_ERR_INVALID_ARGUMENT, "block tables exceed lane");
+        int32_t* h_tbl = h_lrows + L->max_segs;
+        std::memcpy(h_tbl, tbl.data(), tbl.size() * 4);
+        int32_t* h_ditems = h_tbl + L->max_tbl;
+        std::memcpy(h_ditems, ditems.data(), ditems.size() * sizeof(DecodeItem));
+        int32_t* h_pitems = h_ditems + 4 * L->max_segs;
+        std::memcpy(h_pitems, pitems.data(), pitems.size() * sizeof(PrefillItem));
+        const size_t used = size_t(h_pitems - hm) + 4 * pitems.size();
+
+        cudaStream_t st = L->stream;
+        cuda_check(cudaEventRecord(L->ev0, st), "event");
+        cuda_check(cudaMemcpyAsync(L->d_meta, hm, used * 4, cudaMemcpyHostToDevice, st), "meta H2D");
+        const int32_t* d_tok = L->d_meta;
+        const int32_t* d_pos = d_tok + T;
+        const int32_t* d_slot = d_pos + T;
+        const int32_t* d_lrows = d_slot + T;
+        const int32_t* d_tbl = d_lrows + L->max_segs;
+        const DecodeItem* d_ditems = reinterpret_cast<const DecodeItem*>(d_tbl + L->max_tbl);
+        const PrefillItem* d_pitems =
+            reinterpret_cast<const PrefillItem*>(d_tbl + L->max_tbl + 4 * L->max_segs);
+
+        // ---- forward -----------------------------------------------------------------------
+        const int qd = s.hq * s.hd, kvd = s.hkv * s.hd;
+        AttnShape as{};
+        as.hq = s.hq;
+        as.hkv = s.hkv;
+        as.hd = s.hd;
+        as.num_blocks = kv->nb;
+        as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(s.hd)));
+        cuda_check(embed(d_tok, m->embed.ptr, L->x, T, s.d, st), "embed");
+        for (int l = 0; l < s.layers; ++l) {
+            const auto& ly = m->layers[l];
+            as.layer = l;
+            cuda_check(rmsnorm(L->x, nullptr, ly.attn_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
+            linear(L, L->map_h, ly.qkv, T, EPI_BF16, L->qkv, qd + 2 * kvd, ly.qkv_bias, nullptr, nullptr);
+            cuda_check(rope_append(L->qkv, d_pos, d_slot, m->cos_t, m->sin_t, L->q, kv->k_pool,
+                                   kv->v_pool, T, s.hq, s.hkv, s.hd, l, kv->nb, st),
+                       "rope_append");
+            if (!ditems.empty())
+                cuda_check(decode_attention(L->q, kv->k_pool, kv->v_pool, d_ditems, int(ditems.size()),
+                                            max_ctx, d_tbl, L->attn, L->part_o, L->part_ml,
+                                            L->max_splits, m->num_sms, as, st),
+                           "decode attention");
+            if (!pitems.empty())
+                cuda_check(prefill_attention(L->map_q, kv->tk, kv->tv, d_pitems, int(pitems.size()),
+                                             d_tbl, L->attn, as, st),
+                           "prefill attention");
+            linear(L, L->map_attn, ly.o, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
+            cuda_check(rmsnorm(L->x, nullptr, ly.mlp_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
+            linear(L, L->map_h, ly.gate_up, T, EPI_SILU, L->act, s.ffn, nullptr, nullptr, nullptr);
+            linear(L, L->map_act, ly.down, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
+        }
+        if (n_logit > 0) {
+            cuda_check(rmsnorm(L->x, d_lrows, m->final_norm, L->hl, n_logit, s.d, s.eps, st), "final norm");
+            linear(L, L->map_hl, m->lm_head, n_logit, EPI_F32, nullptr, s.vocab, nullptr, nullptr,
+                   L->logits);
+            cuda_check(argmax_rows(L->logits, n_logit, s.vocab, s.vocab, L->d_out, nullptr, st), "argmax");
+            cuda_check(cudaMemcpyAsync(L->h_out, L->d_out, n_logit * 4, cudaMemcpyDeviceToHost, st),
+                       "ids D2H");
+        }
+        cuda_check(cudaEventRecord(L->ev1, st), "event");
+        L->launched = true;
+        L->last_logit_rows = n_logit;
+    });
+}
+
+asb_status asb_lane_fetch(asb_lane* L, int32_t* out_next, int n, float* out_logits) {
+    if (!L) return ASB_ERR_INVALID_ARGUMENT;
+    return guarded([&] {
+        if (!L->launched) fail(ASB_ERR_NO_DATA, "nothing launched on this lane");
+        cuda_check(cudaEventSynchronize(L->ev1), "lane fetch");
+        if (n > L->last_logit_rows) fail(ASB_ERR_INVALID_ARGUMENT, "more ids requested than produced");
+        if (out_next) std::memcpy(out_next, L->h_out, size_t(n) * 4);
+        if (out_logits)
+            cuda_check(cudaMemcpy(out_logits, L->logits, size_t(n) * L->m->spec.vocab * 4,
+                                  cudaMemcpyDeviceToHost),
+                       "logits D2H");
+    });
+}
+
+asb_status asb_prefill_launch(asb_lane* lane, asb_kv* kv, uint32_t session, const int32_t* tokens,
+                              int n) {
+    asb_segment g{session, n, 1};
+    return asb_forward(lane, kv, &g, 1, tokens);
+}
+
+asb_status asb_decode_launch(asb_lane* lane, asb_kv* kv, const uint32_t* sessions,
+                             const int32_t* in_tokens, int batch, int64_t chunk_session,
+                             const int32_t* chunk_tokens, int chunk_n) {
+    std::vector<asb_segment> segs;
+    std::vector<int32_t> toks;
+    for (int i = 0; i < batch; ++i) {
+        segs.push_back(asb_segment{sessions[i], 1, 1});
+        toks.push_back(in_tokens[i]);
+    }
+    if (chunk_session >= 0 && chunk_n > 0) {
+        segs.push_back(asb_segment{static_cast<uint32_t>(chunk_session), chunk_n, 1});
+        toks.insert(toks.end(), chunk_tokens, chunk_tokens + chunk_n);
+    }
+    if (segs.empty()) {
+        g_err = "decode step needs at least one stream or an admitted chunk";
+        return ASB_ERR_INVALID_ARGUMENT;
+    }
+    return asb_forward(lane, kv, segs.data(), int(segs.size()), toks.data());
+}
+
+asb_status asb_debug_gemm(const void* x, const void* w, const void* bias, const void* resid,
+                          void* out, int tokens, int n_out, int k, int epi, int force_path,
+                          int splits, void* stream) {
+    return guarded([&] {
+        Weight W;
+        W.ptr = static_cast<__nv_bfloat16*>(const_cast<void*>(w));
+        W.rows = n_out;
+        W.cols = k;
+        weight_maps(W);
+        CUtensorMap xm[5];
+        act_maps(xm, x, tokens, k);
+        asb_lane tmp;  // only stream, ws and sms are used by linear()
+        asb_model fake;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, dev), "props");
+        fake.device = dev;
+        fake.num_sms = prop.multiProcessorCount;
+        tmp.m = &fake;
+        tmp.stream = static_cast<cudaStream_t>(stream);
+        const int ws_rows = std::min(tokens, 256);
+        cuda_check(cudaMalloc(&tmp.ws, size_t(ws_rows) * n_out * 4), "ws");
+        cuda_check(cudaMemset(tmp.ws, 0, size_t(ws_rows) * n_out * 4), "ws");
+        const int ldo = epi == EPI_SILU ? n_out / 2 : n_out;
+        linear(&tmp, xm, W, tokens, epi, static_cast<__nv_bfloat16*>(out), ldo,
+               static_cast<const __nv_bfloat16*>(bias), static_cast<const __nv_bfloat16*>(resid),
+               epi == EPI_F32 ? static_cast<float*>(out) : nullptr, force_path, splits);
+        cuda_check(cudaStreamSynchronize(tmp.stream), "debug gemm");
+        cudaFree(tmp.ws);
+        tmp.ws = nullptr;
+        tmp.allocs.clear();
+        fake.allocs.clear();
+        tmp.m = &fake;
+        tmp.stream = nullptr;
+        tmp.launched = false;
+    });
+}
+
+}  // extern "C"
