@@ -1,0 +1,182 @@
+#include "devexec.h"
+
+#include <algorithm>
+#include <cstring>
+
+namespace as {
+
+using nlohmann::json;
+
+void DeviceExec::ok(asb_status st, const char* what) const {
+    if (st == ASB_OK) return;
+    const std::string msg = std::string(what) + ": " + asb_last_error();
+    if (st == ASB_ERR_PROTOCOL) raise(Err::Protocol, msg);
+    if (st == ASB_ERR_INFEASIBLE) raise(Err::Infeasible, msg);
+    if (st == ASB_ERR_VALIDATION) raise(Err::Validation, msg);
+    raise(Err::Invalid, msg);
+}
+
+DeviceExec::DeviceExec(const RunCfg& cfg, const std::vector<Plan>& plans) {
+    const BackendCfg& be = cfg.backend;
+    unit_ = be.prefill_unit_tokens;
+    const uint64_t wseed = be.weight_seed ? be.weight_seed : cfg.seed;
+    // longest session context and total KV footprint, from the pre-sampled plans
+    int max_ctx = 0;
+    int64_t blocks = 0;
+    const int bt = asb_kv_block_tokens();
+    for (const auto& p : plans) {
+        int total = p.cold;
+        for (int d : p.decodes) total += d;
+        for (int r : p.resumes) total += r;
+        max_ctx = std::max(max_ctx, total + 1);
+        blocks += (total + bt - 1) / bt + 1;
+    }
+    const int ctx = be.max_context > 0 ? be.max_context : ((max_ctx + 255) / 256) * 256;
+    ok(asb_model_create(be.model.c_str(), wseed, be.device, ctx, &model_), "asb_model_create");
+    char* desc = nullptr;
+    ok(asb_model_describe(model_, &desc), "asb_model_describe");
+    info_ = json::parse(desc);
+    asb_string_free(desc);
+    const int nblocks = be.kv_blocks > 0 ? be.kv_blocks : static_cast<int>(blocks + 8);
+    ok(asb_kv_create(model_, nblocks, &kv_), "asb_kv_create");
+    const int n = static_cast<int>(plans.size());
+    ok(asb_lane_create(model_, n + cfg.exec.resume_chunk + 8, n + 2, nullptr, &dlane_), "decode lane");
+    ok(asb_lane_create(model_, std::max(unit_, 512), 4, nullptr, &plane_), "prefill lane");
+    if (be.clock == Clock::Wall) {
+        const int levels = cfg.profile.slots();
+        int gran = be.green_granularity;
+        if (be.green_contexts) {
+            ok(asb_slots_create(be.device, levels, gran, &slots_), "asb_slots_create");
+            levels_ = levels;
+        }
+    }
+    // token streams
+    const int V = info_["vocab"].get<int>();
+    cold_.resize(plans.size());
+    resume_.resize(plans.size());
+    for (const auto& p : plans) {
+        Stream64 r = Stream64::named(cfg.seed, "tok/" + std::to_string(p.id) + "/cold");
+        auto& c = cold_[p.id];
+        c.resize(static_cast<size_t>(p.cold));
+        for (auto& t : c) t = static_cast<int32_t>(r.below(static_cast<uint64_t>(V)));
+        resume_[p.id].resize(p.resumes.size());
+        for (size_t k = 0; k < p.resumes.size(); ++k) {
+            Stream64 rr = Stream64::named(cfg.seed, "tok/" + std::to_string(p.id) + "/resume/" + std::to_string(k));
+            auto& v = resume_[p.id][k];
+            v.resize(static_cast<size_t>(p.resumes[k]));
+            for (auto& t : v) t = static_cast<int32_t>(rr.below(static_cast<uint64_t>(V)));
+        }
+    }
+    info_["kv_blocks"] = nblocks;
+    info_["prefill_unit_tokens"] = unit_;
+    info_["build"] = asb_build_info();
+    start_clock();
+}
+
+DeviceExec::~DeviceExec() {
+    if (dlane_) asb_lane_free(dlane_);
+    if (plane_) asb_lane_free(plane_);
+    if (slots_) asb_slots_free(slots_);
+    if (kv_) asb_kv_free(kv_);
+    if (model_) asb_model_free(model_);
+}
+
+void DeviceExec::step_launch(const std::vector<Row>& rows, int64_t chunk_s, const int32_t* chunk,
+                             int chunk_n, bool chunk_logits) {
+    std::vector<asb_segment> segs;
+    std::vector<int32_t> toks;
+    segs.reserve(rows.size() + 1);
+    for (const auto& r : rows) {
+        segs.push_back(asb_segment{r.s, 1, 1});
+        toks.push_back(r.tok);
+    }
+    if (chunk_s >= 0 && chunk_n > 0) {
+        segs.push_back(asb_segment{static_cast<uint32_t>(chunk_s), chunk_n, chunk_logits ? 1 : 0});
+        toks.insert(toks.end(), chunk, chunk + chunk_n);
+    }
+    step_logit_rows_ = static_cast<int>(rows.size()) + (chunk_s >= 0 && chunk_n > 0 && chunk_logits ? 1 : 0);
+    ok(asb_forward(dlane_, kv_, segs.data(), static_cast<int>(segs.size()), toks.data()), "decode step");
+}
+
+bool DeviceExec::step_ready() const { return asb_lane_query(dlane_) == 1; }
+
+std::vector<int32_t> DeviceExec::step_collect(float* dev_ms) {
+    std::vector<int32_t> ids(static_cast<size_t>(std::max(step_logit_rows_, 1)));
+    ok(asb_lane_fetch(dlane_, ids.data(), step_logit_rows_, nullptr), "decode fetch");
+    ids.resize(static_cast<size_t>(step_logit_rows_));
+    if (dev_ms) *dev_ms = asb_lane_last_ms(dlane_);
+    return ids;
+}
+
+void DeviceExec::prefill_launch(uint32_t s, const int32_t* toks, int n, bool want) {
+    asb_segment g{s, n, want ? 1 : 0};
+    prefill_want_ = want;
+    ok(asb_forward(plane_, kv_, &g, 1, toks), "prefill unit");
+}
+
+bool DeviceExec::prefill_ready() const { return asb_lane_query(plane_) == 1; }
+
+int32_t DeviceExec::prefill_collect(float* dev_ms) {
+    int32_t id = -1;
+    if (prefill_want_) {
+        ok(asb_lane_fetch(plane_, &id, 1, nullptr), "prefill fetch");
+    } else {
+        ok(asb_lane_wait(plane_), "prefill wait");
+    }
+    if (dev_ms) *dev_ms = asb_lane_last_ms(plane_);
+    return id;
+}
+
+void DeviceExec::bind(int level, bool shared) {
+    if (!slots_) return;
+    const int lvl = shared ? levels_ : level;
+    void *sd = nullptr, *sp = nullptr;
+    ok(asb_slots_bind(slots_, lvl, &sd, &sp), "asb_slots_bind");
+    ok(asb_lane_set_stream(dlane_, sd), "bind decode lane");
+    ok(asb_lane_set_stream(plane_, sp), "bind prefill lane");
+    ok(asb_slots_sm_counts(slots_, lvl, &dsms_, &psms_), "sm counts");
+}
+
+bool DeviceExec::green() const { return slots_ && asb_slots_green(slots_) == 1; }
+
+void DeviceExec::kv_open(uint32_t s) { ok(asb_kv_begin_write(kv_, s), "kv begin_write"); }
+
+void DeviceExec::kv_seal(uint32_t s, int np) {
+    ok(asb_kv_commit(kv_, s, np), "kv commit");
+    const int len = asb_kv_length(kv_, s);
+    if (len != np)
+        raise(Err::Protocol, "device KV holds " + std::to_string(len) + " tokens for session " +
+                                 std::to_string(s) + " at commit of prefix " + std::to_string(np));
+}
+
+void DeviceExec::kv_grow(uint32_t s, int n) {
+    ok(asb_kv_append(kv_, s, n), "kv append");
+    const int len = asb_kv_length(kv_, s), pre = asb_kv_prefix(kv_, s);
+    if (len != pre)
+        raise(Err::Protocol, "device KV holds " + std::to_string(len) + " tokens for session " +
+                                 std::to_string(s) + " but the registry prefix is " + std::to_string(pre));
+}
+
+void DeviceExec::kv_need_sealed(uint32_t s) { ok(asb_kv_require_sealed(kv_, s), "kv require_sealed"); }
+
+int DeviceExec::kv_len(uint32_t s) const { return asb_kv_length(kv_, s); }
+
+void DeviceExec::kv_release(uint32_t s) { ok(asb_kv_release(kv_, s), "kv release"); }
+
+json DeviceExec::describe() const {
+    json j = info_;
+    j["green_contexts"] = green();
+    j["levels"] = levels_;
+    if (slots_) {
+        json lv = json::array();
+        for (int l = 1; l <= levels_; ++l) {
+            int d = 0, p = 0;
+            asb_slots_sm_counts(slots_, l, &d, &p);
+            lv.push_back({{"level", l}, {"decode_sms", d}, {"prefill_sms", p}});
+        }
+        j["partitions"] = lv;
+    }
+    return j;
+}
+
+}  // namespace as
