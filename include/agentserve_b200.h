@@ -121,6 +121,21 @@ asb_status asb_forward(asb_lane* lane, asb_kv* kv, const asb_segment* segs, int 
  * out_logits != NULL, fp32 logits [n][vocab].  Blocks until the launch completes. */
 asb_status asb_lane_fetch(asb_lane* lane, int32_t* out_next, int n, float* out_logits);
 
+/* Kernel timing inside the lane: CUDA events on the lane's stream around every launch of a
+ * category, with the algorithmic work of that launch (bytes for HBM-bound categories,
+ * FLOPs for tensor-bound ones).  Used by bench.py for the live roofline. */
+enum {
+    ASB_STAT_DECODE_ATTN = 0,  /* units: K/V bytes streamed */
+    ASB_STAT_PREFILL_ATTN = 1, /* units: FLOPs */
+    ASB_STAT_DECODE_GEMM = 2,  /* units: weight + activation bytes (swap-AB path) */
+    ASB_STAT_PREFILL_GEMM = 3, /* units: FLOPs */
+    ASB_STAT_FORWARD = 4,      /* whole forward; units: tokens */
+    ASB_STAT_COUNT = 5
+};
+asb_status asb_lane_profile(asb_lane* lane, int enable);
+asb_status asb_lane_stats(asb_lane* lane, int category, double* ms, double* units,
+                          int64_t* launches, int reset);
+
 /* Convenience forms named after the reference seams. */
 asb_status asb_prefill_launch(asb_lane* lane, asb_kv* kv, uint32_t session, const int32_t* tokens,
                               int n);

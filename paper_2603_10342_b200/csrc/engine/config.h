@@ -47,6 +47,7 @@ struct BackendCfg {
     bool green_contexts = true;     // Partitioned policies: SM partitions via green contexts
     int green_granularity = 0;      // SMs per slot on the device; 0: device_sms / total_slots
     bool emit_ids = true;           // record generated token ids in the trace
+    bool profile_kernels = false;   // per-category kernel timing (CUDA events) in the footer
     bool present = false;
     nlohmann::json to_json() const;
 };

@@ -1,11 +1,37 @@
 #include "devexec.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 namespace as {
 
 using nlohmann::json;
+
+struct Resident {
+    std::string key;
+    int ctx = 0, nblocks = 0, dtok = 0, dseg = 0, ptok = 0;
+    asb_model* model = nullptr;
+    asb_kv* kv = nullptr;
+    asb_lane* dlane = nullptr;
+    asb_lane* plane = nullptr;
+    asb_slots* slots = nullptr;
+    int levels = 0;
+    bool busy = false;
+    ~Resident() {
+        if (dlane) asb_lane_free(dlane);
+        if (plane) asb_lane_free(plane);
+        if (slots) asb_slots_free(slots);
+        if (kv) asb_kv_free(kv);
+        if (model) asb_model_free(model);
+    }
+};
+
+namespace {
+std::mutex g_res_mu;
+std::shared_ptr<Resident> g_res;
+}  // namespace
 
 void DeviceExec::ok(asb_status st, const char* what) const {
     if (st == ASB_OK) return;
@@ -32,24 +58,63 @@ DeviceExec::DeviceExec(const RunCfg& cfg, const std::vector<Plan>& plans) {
         blocks += (total + bt - 1) / bt + 1;
     }
     const int ctx = be.max_context > 0 ? be.max_context : ((max_ctx + 255) / 256) * 256;
-    ok(asb_model_create(be.model.c_str(), wseed, be.device, ctx, &model_), "asb_model_create");
+    const int nblocks = be.kv_blocks > 0 ? be.kv_blocks : static_cast<int>(blocks + 8);
+    const int n = static_cast<int>(plans.size());
+    const int dtok = n + cfg.exec.resume_chunk + 8, dseg = n + 2, ptok = std::max(unit_, 512);
+    const int levels = cfg.profile.slots();
+    const bool want_slots = be.clock == Clock::Wall && be.green_contexts;
+    const std::string key = be.model + "|" + std::to_string(wseed) + "|" + std::to_string(be.device) +
+                            "|" + std::to_string(want_slots) + "|" + std::to_string(levels) + "|" +
+                            std::to_string(be.green_granularity);
+    const bool cache_on = std::getenv("AGENTSERVE_NO_CACHE") == nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_res_mu);
+        if (cache_on && g_res && !g_res->busy && g_res->key == key && g_res->ctx >= ctx &&
+            g_res->nblocks >= nblocks && g_res->dtok >= dtok && g_res->dseg >= dseg && g_res->ptok >= ptok) {
+            res_ = g_res;
+            res_->busy = true;
+        }
+    }
+    if (!res_) {
+        auto r = std::make_shared<Resident>();
+        r->key = key;
+        r->ctx = ctx;
+        r->nblocks = nblocks;
+        r->dtok = dtok;
+        r->dseg = dseg;
+        r->ptok = ptok;
+        {
+            // drop an idle cached engine first so two models never coexist needlessly
+            std::lock_guard<std::mutex> lk(g_res_mu);
+            if (g_res && !g_res->busy) g_res.reset();
+        }
+        ok(asb_model_create(be.model.c_str(), wseed, be.device, ctx, &r->model), "asb_model_create");
+        ok(asb_kv_create(r->model, nblocks, &r->kv), "asb_kv_create");
+        ok(asb_lane_create(r->model, dtok, dseg, nullptr, &r->dlane), "decode lane");
+        ok(asb_lane_create(r->model, ptok, 4, nullptr, &r->plane), "prefill lane");
+        if (want_slots) {
+            ok(asb_slots_create(be.device, levels, be.green_granularity, &r->slots), "asb_slots_create");
+            r->levels = levels;
+        }
+        r->busy = true;
+        res_ = r;
+        if (cache_on) {
+            std::lock_guard<std::mutex> lk(g_res_mu);
+            if (!g_res || !g_res->busy) g_res = r;
+        }
+    }
+    model_ = res_->model;
+    kv_ = res_->kv;
+    dlane_ = res_->dlane;
+    plane_ = res_->plane;
+    slots_ = res_->slots;
+    levels_ = res_->levels;
     char* desc = nullptr;
     ok(asb_model_describe(model_, &desc), "asb_model_describe");
     info_ = json::parse(desc);
     asb_string_free(desc);
-    const int nblocks = be.kv_blocks > 0 ? be.kv_blocks : static_cast<int>(blocks + 8);
-    ok(asb_kv_create(model_, nblocks, &kv_), "asb_kv_create");
-    const int n = static_cast<int>(plans.size());
-    ok(asb_lane_create(model_, n + cfg.exec.resume_chunk + 8, n + 2, nullptr, &dlane_), "decode lane");
-    ok(asb_lane_create(model_, std::max(unit_, 512), 4, nullptr, &plane_), "prefill lane");
-    if (be.clock == Clock::Wall) {
-        const int levels = cfg.profile.slots();
-        int gran = be.green_granularity;
-        if (be.green_contexts) {
-            ok(asb_slots_create(be.device, levels, gran, &slots_), "asb_slots_create");
-            levels_ = levels;
-        }
-    }
+    for (const auto& p : plans) sessions_.push_back(p.id);
+    for (uint32_t sid : sessions_) asb_kv_release(kv_, sid);  // a reused pool starts empty
     // token streams
     const int V = info_["vocab"].get<int>();
     cold_.resize(plans.size());
@@ -67,18 +132,30 @@ DeviceExec::DeviceExec(const RunCfg& cfg, const std::vector<Plan>& plans) {
             for (auto& t : v) t = static_cast<int32_t>(rr.below(static_cast<uint64_t>(V)));
         }
     }
-    info_["kv_blocks"] = nblocks;
+    if (be.profile_kernels) {
+        for (int c = 0; c < ASB_STAT_COUNT; ++c) {  // start from zero
+            asb_lane_stats(dlane_, c, nullptr, nullptr, nullptr, 1);
+            asb_lane_stats(plane_, c, nullptr, nullptr, nullptr, 1);
+        }
+        asb_lane_profile(dlane_, 1);
+        asb_lane_profile(plane_, 1);
+        profiling_ = true;
+    }
+    info_["kv_blocks"] = res_->nblocks;
     info_["prefill_unit_tokens"] = unit_;
     info_["build"] = asb_build_info();
     start_clock();
 }
 
 DeviceExec::~DeviceExec() {
-    if (dlane_) asb_lane_free(dlane_);
-    if (plane_) asb_lane_free(plane_);
-    if (slots_) asb_slots_free(slots_);
-    if (kv_) asb_kv_free(kv_);
-    if (model_) asb_model_free(model_);
+    if (!res_) return;
+    asb_lane_wait(dlane_);
+    asb_lane_wait(plane_);
+    for (uint32_t sid : sessions_) asb_kv_release(kv_, sid);
+    asb_lane_profile(dlane_, 0);
+    asb_lane_profile(plane_, 0);
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    res_->busy = false;
 }
 
 void DeviceExec::step_launch(const std::vector<Row>& rows, int64_t chunk_s, const int32_t* chunk,
@@ -165,6 +242,24 @@ void DeviceExec::kv_release(uint32_t s) { ok(asb_kv_release(kv_, s), "kv release
 
 json DeviceExec::describe() const {
     json j = info_;
+    if (profiling_) {
+        static const char* names[ASB_STAT_COUNT] = {"decode_attn", "prefill_attn", "decode_gemm",
+                                                     "prefill_gemm", "forward"};
+        static const char* units[ASB_STAT_COUNT] = {"bytes", "flops", "bytes", "flops", "tokens"};
+        json k = json::object();
+        for (int c = 0; c < ASB_STAT_COUNT; ++c) {
+            json lanes = json::object();
+            for (int which = 0; which < 2; ++which) {
+                double ms = 0.0, u = 0.0;
+                int64_t n = 0;
+                asb_lane_stats(which == 0 ? dlane_ : plane_, c, &ms, &u, &n, 0);
+                lanes[which == 0 ? "decode_lane" : "prefill_lane"] = {{"ms", ms}, {"units", u}, {"launches", n}};
+            }
+            lanes["unit"] = units[c];
+            k[names[c]] = lanes;
+        }
+        j["kernels"] = k;
+    }
     j["green_contexts"] = green();
     j["levels"] = levels_;
     if (slots_) {

@@ -5,6 +5,7 @@
 
 #include <chrono>
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -13,6 +14,11 @@
 #include "json.hpp"
 
 namespace as {
+
+// Device state that outlives one run: weights, KV pool, lanes, green contexts.  Cached
+// process-wide so back-to-back agsv_simulate calls with a compatible backend reuse the
+// resident model instead of re-initialising it (set AGENTSERVE_NO_CACHE=1 to disable).
+struct Resident;
 
 class DeviceExec {
 public:
@@ -67,16 +73,19 @@ public:
 private:
     void ok(asb_status st, const char* what) const;
 
+    std::shared_ptr<Resident> res_;
     asb_model* model_ = nullptr;
     asb_kv* kv_ = nullptr;
     asb_lane* dlane_ = nullptr;
     asb_lane* plane_ = nullptr;
     asb_slots* slots_ = nullptr;
     int levels_ = 0;
+    std::vector<uint32_t> sessions_;
     int dsms_ = 0, psms_ = 0;
     int unit_ = 2048;
     int step_logit_rows_ = 0;
     bool prefill_want_ = false;
+    bool profiling_ = false;
     std::vector<std::vector<int32_t>> cold_;
     std::vector<std::vector<std::vector<int32_t>>> resume_;
     std::chrono::steady_clock::time_point t0_;

@@ -264,6 +264,53 @@ struct asb_lane {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool launched = false;
     int last_logit_rows = 0;
+    // per-category kernel timing (asb_lane_profile / asb_lane_stats)
+    struct Mark {
+        cudaEvent_t a, b;
+        int cat;
+        double units;
+    };
+    bool prof = false;
+    std::vector<Mark> marks;
+    std::vector<cudaEvent_t> pool;
+    double st_ms[ASB_STAT_COUNT] = {}, st_units[ASB_STAT_COUNT] = {};
+    int64_t st_n[ASB_STAT_COUNT] = {};
+
+    cudaEvent_t take_event() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        cuda_check(cudaEventCreate(&e), "event");
+        return e;
+    }
+    template <typename Fn>
+    void timed(int cat, double units, Fn&& fn) {
+        if (!prof) {
+            fn();
+            return;
+        }
+        Mark m{take_event(), take_event(), cat, units};
+        cuda_check(cudaEventRecord(m.a, stream), "event");
+        fn();
+        cuda_check(cudaEventRecord(m.b, stream), "event");
+        marks.push_back(m);
+    }
+    void resolve_marks() {
+        for (auto& m : marks) {
+            float ms = 0.f;
+            if (cudaEventSynchronize(m.b) == cudaSuccess && cudaEventElapsedTime(&ms, m.a, m.b) == cudaSuccess) {
+                st_ms[m.cat] += ms;
+                st_units[m.cat] += m.units;
+                st_n[m.cat] += 1;
+            }
+            pool.push_back(m.a);
+            pool.push_back(m.b);
+        }
+        marks.clear();
+    }
 
     ~asb_lane() {
         cudaSetDevice(m->device);
@@ -273,6 +320,11 @@ struct asb_lane {
         if (h_out) cudaFreeHost(h_out);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        for (auto& m : marks) {
+            cudaEventDestroy(m.a);
+            cudaEventDestroy(m.b);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
         if (own_stream && stream) cudaStreamDestroy(stream);
     }
 };
@@ -306,7 +358,12 @@ void linear(asb_lane* L, const CUtensorMap* xmaps, const Weight& w, int T, int e
     p.ws = L->ws;
     const int num_sms = L->m->num_sms;
     const bool swap = force_path >= 0 ? force_path == 1 : T <= 256;
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
+    // algorithmic work: swap (decode) path is weight-streaming -> bytes; normal -> flops
+    const double units = swap ? 2.0 * (double(w.rows) * w.cols + double(T) * w.cols) +
+                                    double(T) * w.rows * (epi == EPI_F32 ? 4.0 : 2.0)
+                              : 2.0 * T * double(w.rows) * w.cols;
+    L->timed(swap ? ASB_STAT_DECODE_GEMM : ASB_STAT_PREFILL_GEMM, units, [&] {
     if (swap) {
         const int bn = gemm_pick_bn(T);
         p.swap = 1;
@@ -330,6 +387,7 @@ void linear(asb_lane* L, const CUtensorMap* xmaps, const Weight& w, int T, int e
         // normal path: B = W.  bn==128 reuses the box-128 weight map.
         e = gemm_launch(xmaps[0], bn == 256 ? w.map_b256 : w.map_a128, p, bn, num_sms, L->stream);
     }
+    });
     cuda_check(e, "gemm launch");
 }
 
@@ -793,6 +851,16 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         as.hd = s.hd;
         as.num_blocks = kv->nb;
         as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(s.hd)));
+        // algorithmic work per layer: decode attention streams every context token's K and V
+        // once; prefill attention is 4*hd flops per (query, key<=query) pair per head.
+        double dattn_bytes = 0.0, pattn_flops = 0.0;
+        for (const auto& it : ditems) dattn_bytes += double(it.ctx_len) * s.hkv * s.hd * 2 * 2;
+        for (const auto& it : pitems)
+            pattn_flops += 4.0 * s.hd * s.hq *
+                           (double(it.n_q) * it.q_pos0 + double(it.n_q) * (it.n_q + 1) / 2.0);
+        if (L->prof && !L->marks.empty()) L->resolve_marks();
+        cudaEvent_t fwd_a = L->prof ? L->take_event() : nullptr;
+        if (fwd_a) cuda_check(cudaEventRecord(fwd_a, st), "event");
         cuda_check(embed(d_tok, m->embed.ptr, L->x, T, s.d, st), "embed");
         for (int l = 0; l < s.layers; ++l) {
             const auto& ly = m->layers[l];
@@ -803,14 +871,18 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                                    kv->v_pool, T, s.hq, s.hkv, s.hd, l, kv->nb, st),
                        "rope_append");
             if (!ditems.empty())
-                cuda_check(decode_attention(L->q, kv->k_pool, kv->v_pool, d_ditems, int(ditems.size()),
-                                            max_ctx, d_tbl, L->attn, L->part_o, L->part_ml,
-                                            L->max_splits, m->num_sms, as, st),
-                           "decode attention");
+                L->timed(ASB_STAT_DECODE_ATTN, dattn_bytes, [&] {
+                    cuda_check(decode_attention(L->q, kv->k_pool, kv->v_pool, d_ditems, int(ditems.size()),
+                                                max_ctx, d_tbl, L->attn, L->part_o, L->part_ml,
+                                                L->max_splits, m->num_sms, as, st),
+                               "decode attention");
+                });
             if (!pitems.empty())
-                cuda_check(prefill_attention(L->map_q, kv->tk, kv->tv, d_pitems, int(pitems.size()),
-                                             d_tbl, L->attn, as, st),
-                           "prefill attention");
+                L->timed(ASB_STAT_PREFILL_ATTN, pattn_flops, [&] {
+                    cuda_check(prefill_attention(L->map_q, kv->tk, kv->tv, d_pitems, int(pitems.size()),
+                                                 d_tbl, L->attn, as, st),
+                               "prefill attention");
+                });
             linear(L, L->map_attn, ly.o, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
             cuda_check(rmsnorm(L->x, nullptr, ly.mlp_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
             linear(L, L->map_h, ly.gate_up, T, EPI_SILU, L->act, s.ffn, nullptr, nullptr, nullptr);
@@ -824,9 +896,37 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
             cuda_check(cudaMemcpyAsync(L->h_out, L->d_out, n_logit * 4, cudaMemcpyDeviceToHost, st),
                        "ids D2H");
         }
+        if (fwd_a) {
+            cudaEvent_t fwd_b = L->take_event();
+            cuda_check(cudaEventRecord(fwd_b, st), "event");
+            L->marks.push_back(asb_lane::Mark{fwd_a, fwd_b, ASB_STAT_FORWARD, double(T)});
+        }
         cuda_check(cudaEventRecord(L->ev1, st), "event");
         L->launched = true;
         L->last_logit_rows = n_logit;
+    });
+}
+
+asb_status asb_lane_profile(asb_lane* L, int enable) {
+    if (!L) return ASB_ERR_INVALID_ARGUMENT;
+    L->prof = enable != 0;
+    return ASB_OK;
+}
+
+asb_status asb_lane_stats(asb_lane* L, int cat, double* ms, double* units, int64_t* launches,
+                          int reset) {
+    if (!L || cat < 0 || cat >= ASB_STAT_COUNT) return ASB_ERR_INVALID_ARGUMENT;
+    return guarded([&] {
+        if (L->launched) cuda_check(cudaEventSynchronize(L->ev1), "lane stats");
+        L->resolve_marks();
+        if (ms) *ms = L->st_ms[cat];
+        if (units) *units = L->st_units[cat];
+        if (launches) *launches = L->st_n[cat];
+        if (reset) {
+            L->st_ms[cat] = 0.0;
+            L->st_units[cat] = 0.0;
+            L->st_n[cat] = 0;
+        }
     });
 }
 

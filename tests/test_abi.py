@@ -1,0 +1,45 @@
+"""The C-ABI library loads, exports every symbol include/*.h declares, and has no CPU
+fallback (device entry points fail with ASB_ERR_CUDA on a GPU-less host)."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import pytest
+import torch
+
+from paper_2603_10342_b200 import _lib
+from paper_2603_10342_b200.agsv import SYMBOLS
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _declared(header: Path) -> list[str]:
+    text = re.sub(r"/\*.*?\*/", "", header.read_text(), flags=re.S)
+    return sorted(set(re.findall(r"\b((?:asb|agsv)_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.mark.parametrize("header", ["agentsim.h", "agentserve_b200.h"])
+def test_every_declared_symbol_is_exported(built_lib, header):
+    L = _lib.lib()
+    names = _declared(ROOT / "include" / header)
+    assert names, header
+    missing = [n for n in names if getattr(L, n, None) is None]
+    assert not missing, missing
+
+
+def test_agsv_surface_is_the_reference_surface():
+    ref = _declared(ROOT / "include" / "agentsim.h")
+    assert sorted(SYMBOLS) == ref and len(ref) == 27
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the GPU-less failure mode")
+def test_no_cpu_fallback(built_lib):
+    L = _lib.lib()
+    h = C.c_void_p()
+    st = L.asb_model_create(b"tiny", 13, 0, 1024, C.byref(h))
+    assert st == 7, "device entry point must fail loudly without a GPU"
+    assert b"device" in L.asb_last_error() or b"CUDA" in L.asb_last_error().upper()
+
+
+def test_build_info(built_lib):
+    assert _lib.lib().asb_build_info().startswith(b"sm_100a")
