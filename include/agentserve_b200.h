@@ -133,6 +133,12 @@ enum {
     ASB_STAT_COUNT = 5
 };
 asb_status asb_lane_profile(asb_lane* lane, int enable);
+/* SMs available to the lane's current stream (green-context partition); sizes persistent
+ * GEMM grids and split-K.  0 = whole device. */
+asb_status asb_lane_set_sms(asb_lane* lane, int sms);
+/* kernels launched and host<->device bytes moved by the lane since the last reset */
+asb_status asb_lane_counters(asb_lane* lane, int64_t* launches, int64_t* h2d_bytes,
+                             int64_t* d2h_bytes, int reset);
 asb_status asb_lane_stats(asb_lane* lane, int category, double* ms, double* units,
                           int64_t* launches, int reset);
 

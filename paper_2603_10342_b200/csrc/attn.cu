@@ -1,8 +1,10 @@
 // Attention over the paged KV cache.
 //
 // * prefill_attention_kernel (K4/K3 in SURVEY §2.3): causal flash attention for cold and
-//   resume prefills and for the admitted resume chunk inside a decode step.  128 query
-//   rows per CTA; S = Q.K^T and O_blk = P.V run on tcgen05 (accumulators in TMEM),
+//   resume prefills and for the admitted resume chunk inside a decode step.  GQA-packed:
+//   the 128 MMA rows of a CTA are (token, query head) pairs of ONE KV head, so each K/V
+//   block is loaded once for all G query heads (3-D TMA box for Q); split-KV over
+//   gridDim.z when the grid is small.  S = Q.K^T and O_blk = P.V run on tcgen05 (TMEM),
 //   K/V blocks arrive by TMA straight from the paged pool, softmax is one thread per
 //   query row (the TMEM lane it owns).  Replaces the prefill rate x length term of
 //   /root/reference/proj/src/engine.cpp:450-475 and the mu_R chunk term of
@@ -13,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 
 #include "attn.h"
@@ -44,7 +47,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
                              const __grid_constant__ CUtensorMap tmap_v,
                              const PrefillItem* __restrict__ items,
                              const int32_t* __restrict__ tables, __nv_bfloat16* __restrict__ out,
-                             const AttnShape s) {
+                             float* __restrict__ part_o, float* __restrict__ part_ml,
+                             int blocks_per_split, const AttnShape s) {
     using C = PCfg<HD>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
@@ -63,11 +67,25 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
     const PrefillItem it = items[blockIdx.x];
-    const int head = blockIdx.y;
-    const int kvh = head / (s.hq / s.hkv);
-    const int n_kv_blocks = (it.q_pos0 + it.n_q + kBlockTokens - 1) / kBlockTokens;
+    const int kvh = blockIdx.y;
+    const int G = s.hq / s.hkv;
+    const int n_rows = it.n_q * G;  // valid MMA rows: (token, head-in-group)
+    const int total_blocks = (it.q_pos0 + it.n_q + kBlockTokens - 1) / kBlockTokens;
+    // split-KV (gridDim.z > 1): this CTA covers KV blocks [blk0, blk0 + n_kv_blocks)
+    const int blk0 = blockIdx.z * blocks_per_split;
+    const int n_kv_blocks = max(0, min(total_blocks, blk0 + blocks_per_split) - blk0);
+    const bool split = gridDim.z > 1;
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
+    if (n_kv_blocks == 0) {
+        // empty split: neutral partials for the valid rows
+        const size_t base = (static_cast<size_t>(blockIdx.x) * gridDim.y + kvh) * gridDim.z + blockIdx.z;
+        for (int r = threadIdx.x; r < n_rows; r += blockDim.x) {
+            part_ml[(base * 128 + r) * 2 + 0] = -FLT_MAX;
+            part_ml[(base * 128 + r) * 2 + 1] = 0.f;
+        }
+        return;
+    }
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmap_q);
@@ -87,6 +105,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+    // The Q box covers (128 / G) * G rows; the remaining (< G) rows stay zero so their
+    // (discarded) outputs are finite.
+    const int box_rows = (128 / G) * G;
+    for (int i = threadIdx.x; i < C::kHalves * (128 - box_rows) * 8; i += blockDim.x) {
+        const int h = i / ((128 - box_rows) * 8), rem = i % ((128 - box_rows) * 8);
+        reinterpret_cast<uint4*>(sq + h * (128 * 128) + (box_rows + rem / 8) * 128)[rem % 8] = make_uint4(0, 0, 0, 0);
+    }
+    fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -95,17 +121,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
     if (warp == 0) {
         if (elect_one()) {
-            mbar_expect_tx(q_full, C::kQBytes);
+            mbar_expect_tx(q_full, C::kHalves * box_rows * 128);  // full box, incl. OOB fill
 #pragma unroll
             for (int h = 0; h < C::kHalves; ++h)
-                tma_load_2d(sq + h * (128 * 128), &tmap_q, q_full, head * HD + h * 64, it.q_row0);
+                tma_load_3d(sq + h * (128 * 128), &tmap_q, q_full, h * 64, kvh * G, it.q_row0);
             const uint64_t pol = policy_evict_last();  // K/V blocks are re-read by other heads
             for (int j = 0; j < n_kv_blocks; ++j) {
                 const int st = j % kKvStages;
                 const uint32_t ph = (j / kKvStages) & 1;
                 mbar_wait(&kv_empty[st], ph ^ 1);
                 mbar_expect_tx(&kv_full[st], C::kStageBytes);
-                const int blk = table[j];
+                const int blk = table[blk0 + j];
                 const int row =
                     ((s.layer * s.num_blocks + blk) * s.hkv + kvh) * kBlockTokens;
                 uint8_t* kdst = skv + st * C::kStageBytes;
@@ -175,7 +201,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         // Softmax / correction warps: one query row per thread.
         const uint32_t quarter = warp & 3;
         const int r = quarter * 32 + lane;
-        const int qpos = it.q_pos0 + r;
+        const int qpos = it.q_pos0 + r / G;  // row r = (token r / G, head kvh*G + r % G)
         const uint32_t t_lane = tmem + ((quarter * 32u) << 16);
         float o[HD];
 #pragma unroll
@@ -193,7 +219,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             tc_fence_before();
             mbar_arrive(&s_free[sb]);
             // mask + scale (log2 domain)
-            const int kbase = j * kBlockTokens;
+            const int kbase = (blk0 + j) * kBlockTokens;
             float mx = m_run;
             float sv[64];
 #pragma unroll
@@ -256,10 +282,21 @@ __global__ void __launch_bounds__(kPThreads, 1)
             for (int e = 0; e < 32; ++e) o[c + e] = o[c + e] * alpha_prev + __uint_as_float(ov[e]);
         }
         tc_fence_before();
-        if (r < it.n_q) {
+        if (split) {
+            if (r < n_rows) {
+                const size_t base =
+                    ((static_cast<size_t>(blockIdx.x) * gridDim.y + kvh) * gridDim.z + blockIdx.z) * 128 + r;
+                float4* po = reinterpret_cast<float4*>(part_o + base * HD);
+#pragma unroll
+                for (int c = 0; c < HD / 4; ++c)
+                    po[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+                part_ml[base * 2 + 0] = m_run;
+                part_ml[base * 2 + 1] = l_run;
+            }
+        } else if (r < n_rows) {
             const float inv = 1.f / l_run;
             uint4* dst = reinterpret_cast<uint4*>(
-                out + static_cast<size_t>(it.q_row0 + r) * (s.hq * HD) + head * HD);
+                out + static_cast<size_t>(it.q_row0 + r / G) * (s.hq * HD) + (kvh * G + r % G) * HD);
 #pragma unroll
             for (int c = 0; c < HD / 8; ++c) {
                 uint4 v;
@@ -522,10 +559,37 @@ __global__ void decode_combine_kernel(const DecodeItem* __restrict__ items,
     out[static_cast<size_t>(items[row].q_row) * hq * HD + h * HD + d] = __float2bfloat16_rn(o / l);
 }
 
+// Merge split-KV partials of prefill rows.  grid = (n_items, hkv, 128 rows), block = HD.
+template <int HD>
+__global__ void prefill_combine_kernel(const PrefillItem* __restrict__ items,
+                                       const float* __restrict__ part_o,
+                                       const float* __restrict__ part_ml, int splits,
+                                       __nv_bfloat16* __restrict__ out, int hq, int hkv) {
+    const PrefillItem it = items[blockIdx.x];
+    const int G = hq / hkv;
+    const int r = blockIdx.z, kvh = blockIdx.y, d = threadIdx.x;
+    if (r >= it.n_q * G) return;
+    const size_t base = (static_cast<size_t>(blockIdx.x) * hkv + kvh) * splits;
+    float m = -FLT_MAX;
+    for (int sp = 0; sp < splits; ++sp) m = fmaxf(m, part_ml[((base + sp) * 128 + r) * 2]);
+    float l = 0.f, o = 0.f;
+    for (int sp = 0; sp < splits; ++sp) {
+        const size_t row = (base + sp) * 128 + r;
+        const float ls = part_ml[row * 2 + 1];
+        if (ls == 0.f) continue;
+        const float w = exp2f(part_ml[row * 2] - m);
+        l += ls * w;
+        o += part_o[row * HD + d] * w;
+    }
+    out[static_cast<size_t>(it.q_row0 + r / G) * hq * HD + (kvh * G + r % G) * HD + d] =
+        __float2bfloat16_rn(o / l);
+}
+
 template <int HD>
 cudaError_t prefill_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                           const PrefillItem* items, int n_items, const int32_t* tables,
-                           __nv_bfloat16* out, const AttnShape& s, cudaStream_t stream) {
+                           const PrefillItem* items, int n_items, int max_blocks, int splits,
+                           const int32_t* tables, __nv_bfloat16* out, float* part_o, float* part_ml,
+                           const AttnShape& s, cudaStream_t stream) {
     using C = PCfg<HD>;
     static bool attr = false;
     if (!attr) {
@@ -534,23 +598,43 @@ cudaError_t prefill_launch(const CUtensorMap& tq, const CUtensorMap& tk, const C
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    dim3 grid(n_items, s.hq);
+    const int bps = (max_blocks + splits - 1) / splits;
+    splits = (max_blocks + bps - 1) / bps;
+    dim3 grid(n_items, s.hkv, splits);
     prefill_attention_kernel<HD><<<grid, kPThreads, C::kSmem, stream>>>(tq, tk, tv, items, tables,
-                                                                       out, s);
+                                                                       out, part_o, part_ml, bps, s);
+    if (splits > 1)
+        prefill_combine_kernel<HD><<<dim3(n_items, s.hkv, 128), HD, 0, stream>>>(
+            items, part_o, part_ml, splits, out, s.hq, s.hkv);
     return cudaGetLastError();
 }
 
 }  // namespace
 
+int prefill_tokens_per_tile(int hq, int hkv) { return 128 / (hq / hkv); }
+
+int prefill_splits(int n_items, int hkv, int max_blocks, int num_sms, size_t ws_rows) {
+    // split the KV range only when the (item, kv head) grid leaves SMs idle
+    const int ctas = n_items * hkv;
+    int splits = (2 * num_sms + ctas - 1) / ctas;
+    splits = std::min(splits, std::max(1, max_blocks / 2));
+    splits = std::min(splits, 32);
+    while (splits > 1 && static_cast<size_t>(ctas) * splits * 128 > ws_rows) --splits;
+    return std::max(splits, 1);
+}
+
 cudaError_t prefill_attention(const CUtensorMap& tmap_q, const CUtensorMap& tmap_k,
                               const CUtensorMap& tmap_v, const PrefillItem* items, int n_items,
-                              const int32_t* tables, __nv_bfloat16* out, const AttnShape& s,
+                              int max_blocks, int splits, const int32_t* tables,
+                              __nv_bfloat16* out, float* part_o, float* part_ml, const AttnShape& s,
                               cudaStream_t stream) {
     if (n_items <= 0) return cudaSuccess;
     if (s.hd == 128)
-        return prefill_launch<128>(tmap_q, tmap_k, tmap_v, items, n_items, tables, out, s, stream);
+        return prefill_launch<128>(tmap_q, tmap_k, tmap_v, items, n_items, max_blocks, splits, tables,
+                                   out, part_o, part_ml, s, stream);
     if (s.hd == 64)
-        return prefill_launch<64>(tmap_q, tmap_k, tmap_v, items, n_items, tables, out, s, stream);
+        return prefill_launch<64>(tmap_q, tmap_k, tmap_v, items, n_items, max_blocks, splits, tables,
+                                  out, part_o, part_ml, s, stream);
     return cudaErrorInvalidValue;
 }
 

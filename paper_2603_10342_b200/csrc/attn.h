@@ -13,11 +13,12 @@ namespace asb {
 // a single TMA box for prefill attention and a 128-bit-coalesced stream for decode.
 constexpr int kBlockTokens = 64;
 
-// One prefill-attention work item: up to 128 query rows of one segment.
+// One prefill-attention work item: up to prefill_tokens_per_tile() query tokens of one
+// segment; the CTA's 128 MMA rows are those tokens x the G query heads of one KV head.
 struct PrefillItem {
-    int q_row0;     // first row in the q / out buffers
-    int q_pos0;     // absolute position of that row
-    int n_q;        // valid query rows (<= 128)
+    int q_row0;     // first token row in the q / out buffers
+    int q_pos0;     // absolute position of that token
+    int n_q;        // valid query tokens (<= 128 / G)
     int table_off;  // offset of this segment's block table in the batch table array
 };
 
@@ -36,9 +37,15 @@ struct AttnShape {
     float scale_log2; // log2(e) / sqrt(hd)
 };
 
+// grid = (items, hkv, splits).  Split-KV over gridDim.z when the grid is small (resume
+// chunks): partials part_o [items*hkv*splits*128][hd] fp32 and part_ml [..][2], merged by a
+// combine kernel.  tmap_q is the 3-D map [T][hq][hd] with box [tokens_per_tile][G][64].
+int prefill_tokens_per_tile(int hq, int hkv);
+int prefill_splits(int n_items, int hkv, int max_blocks, int num_sms, size_t ws_rows);
 cudaError_t prefill_attention(const CUtensorMap& tmap_q, const CUtensorMap& tmap_k,
                               const CUtensorMap& tmap_v, const PrefillItem* items, int n_items,
-                              const int32_t* tables, __nv_bfloat16* out, const AttnShape& s,
+                              int max_blocks, int splits, const int32_t* tables,
+                              __nv_bfloat16* out, float* part_o, float* part_ml, const AttnShape& s,
                               cudaStream_t stream);
 
 // Split-K paged decode attention. partial_* workspaces are sized by the caller for

@@ -327,7 +327,17 @@ std::vector<Plan> make_plans(const WorkloadCfg& w, uint64_t seed) {
             p.resumes.push_back(res.draw(r));
             p.tools.push_back(par.tool.draw(r));
         }
+        p.gid = p.id;
         out.push_back(std::move(p));
+    }
+    if (w.shard_count > 1) {
+        std::vector<Plan> mine;
+        for (auto& p : out)
+            if (static_cast<int>(p.gid % static_cast<uint32_t>(w.shard_count)) == w.shard_index) {
+                p.id = static_cast<uint32_t>(mine.size());
+                mine.push_back(std::move(p));
+            }
+        out = std::move(mine);
     }
     return out;
 }

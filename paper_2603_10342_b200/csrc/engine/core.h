@@ -149,6 +149,7 @@ const char* stage_label(Stage s);
 
 struct Plan {
     uint32_t id = 0;
+    uint32_t gid = 0;  // id in the global (unsharded) workload: names its token streams
     Stage stage = Stage::WaitCold;
     int cached = 0;
     int rounds = 0;
@@ -170,6 +171,8 @@ struct WorkloadCfg {
     std::optional<LenRange> cold, resume, decode;
     std::optional<int> rounds;
     std::optional<ToolDelay> tool;
+    // replica sharding (multi-GPU): keep sessions with gid % shard_count == shard_index
+    int shard_index = 0, shard_count = 1;
     Paradigm resolve() const;
 };
 

@@ -115,18 +115,22 @@ DeviceExec::DeviceExec(const RunCfg& cfg, const std::vector<Plan>& plans) {
     asb_string_free(desc);
     for (const auto& p : plans) sessions_.push_back(p.id);
     for (uint32_t sid : sessions_) asb_kv_release(kv_, sid);  // a reused pool starts empty
+    asb_lane_counters(dlane_, nullptr, nullptr, nullptr, 1);
+    asb_lane_counters(plane_, nullptr, nullptr, nullptr, 1);
+    asb_lane_set_sms(dlane_, 0);
+    asb_lane_set_sms(plane_, 0);
     // token streams
     const int V = info_["vocab"].get<int>();
     cold_.resize(plans.size());
     resume_.resize(plans.size());
     for (const auto& p : plans) {
-        Stream64 r = Stream64::named(cfg.seed, "tok/" + std::to_string(p.id) + "/cold");
+        Stream64 r = Stream64::named(cfg.seed, "tok/" + std::to_string(p.gid) + "/cold");
         auto& c = cold_[p.id];
         c.resize(static_cast<size_t>(p.cold));
         for (auto& t : c) t = static_cast<int32_t>(r.below(static_cast<uint64_t>(V)));
         resume_[p.id].resize(p.resumes.size());
         for (size_t k = 0; k < p.resumes.size(); ++k) {
-            Stream64 rr = Stream64::named(cfg.seed, "tok/" + std::to_string(p.id) + "/resume/" + std::to_string(k));
+            Stream64 rr = Stream64::named(cfg.seed, "tok/" + std::to_string(p.gid) + "/resume/" + std::to_string(k));
             auto& v = resume_[p.id][k];
             v.resize(static_cast<size_t>(p.resumes[k]));
             for (auto& t : v) t = static_cast<int32_t>(rr.below(static_cast<uint64_t>(V)));
@@ -212,6 +216,8 @@ void DeviceExec::bind(int level, bool shared) {
     ok(asb_lane_set_stream(dlane_, sd), "bind decode lane");
     ok(asb_lane_set_stream(plane_, sp), "bind prefill lane");
     ok(asb_slots_sm_counts(slots_, lvl, &dsms_, &psms_), "sm counts");
+    ok(asb_lane_set_sms(dlane_, green() ? dsms_ : 0), "lane sms");
+    ok(asb_lane_set_sms(plane_, green() ? psms_ : 0), "lane sms");
 }
 
 bool DeviceExec::green() const { return slots_ && asb_slots_green(slots_) == 1; }
@@ -242,6 +248,12 @@ void DeviceExec::kv_release(uint32_t s) { ok(asb_kv_release(kv_, s), "kv release
 
 json DeviceExec::describe() const {
     json j = info_;
+    {
+        int64_t l0 = 0, h0 = 0, d0 = 0, l1 = 0, h1 = 0, d1 = 0;
+        asb_lane_counters(dlane_, &l0, &h0, &d0, 0);
+        asb_lane_counters(plane_, &l1, &h1, &d1, 0);
+        j["io"] = {{"kernel_launches", l0 + l1}, {"h2d_bytes", h0 + h1}, {"d2h_bytes", d0 + d1}};
+    }
     if (profiling_) {
         static const char* names[ASB_STAT_COUNT] = {"decode_attn", "prefill_attn", "decode_gemm",
                                                      "prefill_gemm", "forward"};

@@ -252,7 +252,8 @@ struct asb_lane {
     bool own_stream = false;
     int max_T = 0, max_segs = 0, max_tbl = 0, max_pitems = 0, max_splits = 16;
     __nv_bfloat16 *x, *h, *qkv, *q, *attn, *act, *hl;
-    float *logits, *ws, *part_o, *part_ml;
+    float *logits, *ws, *part_o, *part_ml, *ppart_o, *ppart_ml;
+    size_t ppart_rows = 0;
     int32_t* d_meta = nullptr;
     int32_t* h_meta = nullptr;
     int32_t* d_out = nullptr;
@@ -275,6 +276,9 @@ struct asb_lane {
     std::vector<cudaEvent_t> pool;
     double st_ms[ASB_STAT_COUNT] = {}, st_units[ASB_STAT_COUNT] = {};
     int64_t st_n[ASB_STAT_COUNT] = {};
+    int sms = 0;  // SMs of the partition the lane's stream runs on (0: whole device)
+    int64_t n_launch = 0, h2d = 0, d2h = 0;
+    int n_sms() const { return sms > 0 ? sms : m->num_sms; }
 
     cudaEvent_t take_event() {
         if (!pool.empty()) {
@@ -356,7 +360,8 @@ void linear(asb_lane* L, const CUtensorMap* xmaps, const Weight& w, int T, int e
     p.resid = resid;
     p.ldr = ldo;
     p.ws = L->ws;
-    const int num_sms = L->m->num_sms;
+    const int num_sms = L->n_sms();
+    L->n_launch += 1;
     const bool swap = force_path >= 0 ? force_path == 1 : T <= 256;
     cudaError_t e = cudaSuccess;
     // algorithmic work: swap (decode) path is weight-streaming -> bytes; normal -> flops
@@ -685,7 +690,7 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->max_T = max_tokens;
         L->max_segs = std::min(max_segments, max_tokens);
         L->max_tbl = L->max_segs * ((m->max_ctx + kBlockTokens - 1) / kBlockTokens);
-        L->max_pitems = max_tokens / 128 + L->max_segs;
+        L->max_pitems = max_tokens / prefill_tokens_per_tile(s.hq, s.hkv) + L->max_segs;
         if (stream) {
             L->stream = static_cast<cudaStream_t>(stream);
         } else {
@@ -712,6 +717,10 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
             dmalloc(size_t(dec_rows) * s.hq * L->max_splits * s.hd * 4, L->allocs));
         L->part_ml = static_cast<float*>(
             dmalloc(size_t(dec_rows) * s.hq * L->max_splits * 2 * 4, L->allocs));
+        // split-KV partials for small prefill grids (resume chunks): <= 4096 rows of 128 queries
+        L->ppart_rows = size_t(4096) * 128 / 16;
+        L->ppart_o = static_cast<float*>(dmalloc(L->ppart_rows * s.hd * 4, L->allocs));
+        L->ppart_ml = static_cast<float*>(dmalloc(L->ppart_rows * 2 * 4, L->allocs));
         L->meta_ints = size_t(3) * T + L->max_segs + L->max_tbl + 4 * size_t(L->max_segs) +
                        4 * size_t(L->max_pitems) + 64;
         L->d_meta = static_cast<int32_t*>(dmalloc(L->meta_ints * 4, L->allocs));
@@ -722,8 +731,11 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         act_maps(L->map_attn, L->attn, T, qd);
         act_maps(L->map_act, L->act, T, s.ffn);
         act_maps(L->map_hl, L->hl, L->max_segs, s.d);
-        if (!make_tmap_bf16(&L->map_q, L->q, T, qd, qd, 128))
-            fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for q");
+        {
+            const int G = s.hq / s.hkv;
+            if (!make_tmap_bf16_3d(&L->map_q, L->q, s.hd, s.hq, T, G, prefill_tokens_per_tile(s.hq, s.hkv)))
+                fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for q");
+        }
         cuda_check(cudaEventCreate(&L->ev0), "event");
         cuda_check(cudaEventCreate(&L->ev1), "event");
         cuda_check(cudaDeviceSynchronize(), "lane init");
@@ -793,7 +805,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         std::vector<int32_t> tbl;
         std::vector<DecodeItem> ditems;
         std::vector<PrefillItem> pitems;
-        int max_ctx = 0;
+        int max_ctx = 0, max_pblocks = 0;
         int row = 0;
         for (int i = 0; i < n_segs; ++i) {
             const asb_segment& g = segs[i];
@@ -815,8 +827,10 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                 ditems.push_back(DecodeItem{row, start + 1, toff, 0});
                 max_ctx = std::max(max_ctx, start + 1);
             } else {
-                for (int q0 = 0; q0 < g.n_tokens; q0 += 128)
-                    pitems.push_back(PrefillItem{row + q0, start + q0, std::min(128, g.n_tokens - q0), toff});
+                const int tpt = prefill_tokens_per_tile(s.hq, s.hkv);
+                for (int q0 = 0; q0 < g.n_tokens; q0 += tpt)
+                    pitems.push_back(PrefillItem{row + q0, start + q0, std::min(tpt, g.n_tokens - q0), toff});
+                max_pblocks = std::max(max_pblocks, (start + g.n_tokens + kBlockTokens - 1) / kBlockTokens);
             }
             if (g.want_logits) h_lrows[n_logit++] = row + g.n_tokens - 1;
             ss.len = start + g.n_tokens;
@@ -834,6 +848,11 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         cudaStream_t st = L->stream;
         cuda_check(cudaEventRecord(L->ev0, st), "event");
         cuda_check(cudaMemcpyAsync(L->d_meta, hm, used * 4, cudaMemcpyHostToDevice, st), "meta H2D");
+        L->h2d += int64_t(used) * 4;
+        // kernels per forward: embed + per layer (2 norms, rope, 4 GEMMs (+finalize), attention
+        // (decode: 2, prefill: 1)) + final norm / LM head / argmax
+        L->n_launch += 1 + int64_t(s.layers) * (3 + (ditems.empty() ? 0 : 2) + (pitems.empty() ? 0 : 1)) +
+                       (n_logit > 0 ? 2 : 0);
         const int32_t* d_tok = L->d_meta;
         const int32_t* d_pos = d_tok + T;
         const int32_t* d_slot = d_pos + T;
@@ -854,6 +873,9 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         // algorithmic work per layer: decode attention streams every context token's K and V
         // once; prefill attention is 4*hd flops per (query, key<=query) pair per head.
         double dattn_bytes = 0.0, pattn_flops = 0.0;
+        const int psplits = pitems.empty() ? 1
+                                           : prefill_splits(int(pitems.size()), s.hkv, max_pblocks,
+                                                            L->n_sms(), L->ppart_rows);
         for (const auto& it : ditems) dattn_bytes += double(it.ctx_len) * s.hkv * s.hd * 2 * 2;
         for (const auto& it : pitems)
             pattn_flops += 4.0 * s.hd * s.hq *
@@ -874,13 +896,14 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                 L->timed(ASB_STAT_DECODE_ATTN, dattn_bytes, [&] {
                     cuda_check(decode_attention(L->q, kv->k_pool, kv->v_pool, d_ditems, int(ditems.size()),
                                                 max_ctx, d_tbl, L->attn, L->part_o, L->part_ml,
-                                                L->max_splits, m->num_sms, as, st),
+                                                L->max_splits, L->n_sms(), as, st),
                                "decode attention");
                 });
             if (!pitems.empty())
                 L->timed(ASB_STAT_PREFILL_ATTN, pattn_flops, [&] {
                     cuda_check(prefill_attention(L->map_q, kv->tk, kv->tv, d_pitems, int(pitems.size()),
-                                                 d_tbl, L->attn, as, st),
+                                                 max_pblocks, psplits, d_tbl, L->attn, L->ppart_o,
+                                                 L->ppart_ml, as, st),
                                "prefill attention");
                 });
             linear(L, L->map_attn, ly.o, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
@@ -895,6 +918,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
             cuda_check(argmax_rows(L->logits, n_logit, s.vocab, s.vocab, L->d_out, nullptr, st), "argmax");
             cuda_check(cudaMemcpyAsync(L->h_out, L->d_out, n_logit * 4, cudaMemcpyDeviceToHost, st),
                        "ids D2H");
+            L->d2h += int64_t(n_logit) * 4;
         }
         if (fwd_a) {
             cudaEvent_t fwd_b = L->take_event();
@@ -905,6 +929,22 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         L->launched = true;
         L->last_logit_rows = n_logit;
     });
+}
+
+asb_status asb_lane_set_sms(asb_lane* L, int sms) {
+    if (!L || sms < 0) return ASB_ERR_INVALID_ARGUMENT;
+    L->sms = sms;
+    return ASB_OK;
+}
+
+asb_status asb_lane_counters(asb_lane* L, int64_t* launches, int64_t* h2d_bytes, int64_t* d2h_bytes,
+                             int reset) {
+    if (!L) return ASB_ERR_INVALID_ARGUMENT;
+    if (launches) *launches = L->n_launch;
+    if (h2d_bytes) *h2d_bytes = L->h2d;
+    if (d2h_bytes) *d2h_bytes = L->d2h;
+    if (reset) L->n_launch = L->h2d = L->d2h = 0;
+    return ASB_OK;
 }
 
 asb_status asb_lane_profile(asb_lane* L, int enable) {

@@ -128,6 +128,20 @@ class Lane:
     def last_ms(self) -> float:
         return float(lib().asb_lane_last_ms(self.h))
 
+    CATS = ("decode_attn", "prefill_attn", "decode_gemm", "prefill_gemm", "forward")
+
+    def profile(self, on: bool = True) -> None:
+        check(lib().asb_lane_profile(self.h, 1 if on else 0))
+
+    def stats(self, reset: bool = True) -> dict:
+        """{category: (ms, units, launches)} since the last reset (CUDA-event timed)."""
+        out = {}
+        for i, name in enumerate(self.CATS):
+            ms, u, n = C.c_double(), C.c_double(), C.c_int64()
+            check(lib().asb_lane_stats(self.h, i, C.byref(ms), C.byref(u), C.byref(n), 1 if reset else 0))
+            out[name] = (ms.value, u.value, n.value)
+        return out
+
     def close(self):
         if self.h:
             lib().asb_lane_free(self.h)

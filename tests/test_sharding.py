@@ -1,0 +1,62 @@
+"""Multi-GPU = session-sharded replicas with no collective.  Sharding must
+partition the global workload exactly (plans are independent of the shard count because
+every session draws from its own named sub-stream), and bench.py under torchrun (gloo,
+world size 2, virtual clock on CPU) must aggregate into one whole-job JSON line."""
+import json
+import os
+import socket
+import subprocess
+import sys
+import tempfile
+from pathlib import Path
+
+from paper_2603_10342_b200.agsv import Agsv
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _sessions(api, cfg):
+    td = tempfile.mkdtemp()
+    return [json.loads(x) for x in api.run(cfg).jsonl(td).splitlines() if '"rec":"session"' in x]
+
+
+def test_shards_partition_the_global_workload(built_lib):
+    api = Agsv()
+    base = {"workload": {"paradigm": "react", "concurrency": 12}, "policy": "agentserve", "seed": 13}
+    full = _sessions(api, base)
+    for n in (2, 3, 4):
+        seen = {}
+        for r in range(n):
+            cfg = json.loads(json.dumps(base))
+            cfg["workload"].update({"shard_index": r, "shard_count": n})
+            for k, s in enumerate(_sessions(api, cfg)):
+                gid = r + k * n
+                seen[gid] = s
+        assert sorted(seen) == list(range(12))
+        for gid, s in seen.items():
+            g = full[gid]
+            for key in ("arrival", "cold_len", "decode_lens", "resume_lens", "tool_delays", "rounds"):
+                assert s[key] == g[key], (n, gid, key)
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_bench_torchrun_gloo_two_ranks(built_lib):
+    env = dict(os.environ, BENCH_BACKEND="gloo", PYTHONPATH=str(ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"),
+           "--gpus", "2", "--steps", "1", "--warmup", "1", "--sim-clock", "--no-cpu"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    assert d["latency_ms"]["sessions"] == 16  # 8 agents per rank, both ranks counted
+    assert d["value"] > 0
