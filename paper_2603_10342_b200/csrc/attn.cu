@@ -9,9 +9,7 @@
 //   query row (the TMEM lane it owns).  Replaces the prefill rate x length term of
 //   /root/reference/proj/src/engine.cpp:450-475 and the mu_R chunk term of
 //   /root/reference/proj/src/executor.cpp:216-218.
-// * decode_attention_kernel (K2): one query token per row, all GQA heads of one KV head
-//   per CTA, split-K over KV blocks, cp.async double-buffered 128-bit loads, warp-shuffle
-//   softmax.  HBM-bound; replaces the mu_D term of executor.cpp:213-215.
+// Decode attention (K2) lives in decode_attn.cu.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -316,249 +314,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
 }
 
-// ============================================================================ decode
-constexpr int kDThreads = 128;
-constexpr int kMaxGroup = 8;
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int HD>
-__global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ q,
-                                        const __nv_bfloat16* __restrict__ k_pool,
-                                        const __nv_bfloat16* __restrict__ v_pool,
-                                        const DecodeItem* __restrict__ items,
-                                        const int32_t* __restrict__ tables, float* __restrict__ part_o,
-                                        float* __restrict__ part_ml, int blocks_per_split, AttnShape s);
-
-template <int HD>
-struct DCfg {
-    static constexpr int kRow = HD + 8;  // padded smem row (bf16) -> conflict-free 16B reads
-    static constexpr int kTile = kBlockTokens * kRow;  // elements per K (or V) tile
-    static constexpr int kSmem = 4 * kTile * 2 + kMaxGroup * HD * 4 + kMaxGroup * kBlockTokens * 4;
-};
-
-template <int HD>
-cudaError_t decode_prepare() {
-    static bool done = false;
-    if (done) return cudaSuccess;
-    done = true;
-    return cudaFuncSetAttribute(decode_attention_kernel<HD>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, DCfg<HD>::kSmem);
-}
-
-// grid = (n_items, hkv, splits); each CTA: all G query heads of one KV head, a range
-// of KV blocks.  Writes un-normalised partial O plus (m, l) per head.
-template <int HD>
-__global__ void __launch_bounds__(kDThreads)
-    decode_attention_kernel(const __nv_bfloat16* __restrict__ q,
-                            const __nv_bfloat16* __restrict__ k_pool,
-                            const __nv_bfloat16* __restrict__ v_pool,
-                            const DecodeItem* __restrict__ items,
-                            const int32_t* __restrict__ tables, float* __restrict__ part_o,
-                            float* __restrict__ part_ml, int blocks_per_split, AttnShape s) {
-    using C = DCfg<HD>;
-    extern __shared__ __align__(16) uint8_t dsmem[];
-    auto sk = reinterpret_cast<__nv_bfloat16(*)[C::kTile]>(dsmem);
-    auto sv = reinterpret_cast<__nv_bfloat16(*)[C::kTile]>(dsmem + 2 * C::kTile * 2);
-    auto sq = reinterpret_cast<float(*)[HD]>(dsmem + 4 * C::kTile * 2);
-    auto sp = reinterpret_cast<float(*)[kBlockTokens]>(dsmem + 4 * C::kTile * 2 +
-                                                         kMaxGroup * HD * 4);
-    __shared__ float s_alpha[kMaxGroup], s_m[kMaxGroup], s_l[kMaxGroup];
-
-    const DecodeItem it = items[blockIdx.x];
-    const int kvh = blockIdx.y;
-    const int split = blockIdx.z;
-    const int G = s.hq / s.hkv;
-    const int tid = threadIdx.x;
-    const int n_blocks = (it.ctx_len + kBlockTokens - 1) / kBlockTokens;
-    const int b0 = split * blocks_per_split;
-    const int b1 = min(n_blocks, b0 + blocks_per_split);
-    const int32_t* table = tables + it.table_off;
-    const size_t head_tile = static_cast<size_t>(kBlockTokens) * HD;
-
-    // q (bf16) -> fp32 smem, pre-scaled into the log2 domain
-    for (int i = tid; i < G * HD; i += kDThreads) {
-        const int g = i / HD, d = i % HD;
-        sq[g][d] = __bfloat162float(
-                       q[static_cast<size_t>(it.q_row) * s.hq * HD + (kvh * G + g) * HD + d]) *
-                   s.scale_log2;
-    }
-    if (tid < kMaxGroup) {
-        s_m[tid] = -FLT_MAX;
-        s_l[tid] = 0.f;
-    }
-
-    auto load_block = [&](int b, int buf) {
-        const int blk = table[b];
-        const size_t base = ((static_cast<size_t>(s.layer) * s.num_blocks + blk) * s.hkv + kvh) *
-                            head_tile;
-        const __nv_bfloat16* ks = k_pool + base;
-        const __nv_bfloat16* vs = v_pool + base;
-        constexpr int kChunks = kBlockTokens * HD / 8;  // 16-byte chunks per tile
-#pragma unroll
-        for (int c = tid; c < kChunks; c += kDThreads) {
-            const int row = c / (HD / 8), col = (c % (HD / 8)) * 8;
-            cp_async16(&sk[buf][row * C::kRow + col], ks + row * HD + col);
-            cp_async16(&sv[buf][row * C::kRow + col], vs + row * HD + col);
-        }
-        cp_async_commit();
-    };
-
-    // thread ownership
-    const int key = tid & (kBlockTokens - 1);
-    const int hgrp = tid >> 6;  // 0 / 1: heads hgrp, hgrp+2, ...
-    constexpr int kOutPerPass = kDThreads / HD;  // 1 (HD=128) or 2 (HD=64)
-    const int od = tid % HD;
-    const int ogrp = tid / HD;
-    float acc[kMaxGroup];
-#pragma unroll
-    for (int g = 0; g < kMaxGroup; ++g) acc[g] = 0.f;
-
-    if (b0 < b1) load_block(b0, 0);
-    __syncthreads();
-    for (int b = b0; b < b1; ++b) {
-        const int buf = (b - b0) & 1;
-        if (b + 1 < b1) {
-            load_block(b + 1, buf ^ 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        // scores
-        const int kpos = b * kBlockTokens + key;
-        const __nv_bfloat16* krow = &sk[buf][key * C::kRow];
-        float sc[kMaxGroup / 2];
-#pragma unroll
-        for (int i = 0; i < kMaxGroup / 2; ++i) sc[i] = 0.f;
-#pragma unroll 4
-        for (int d = 0; d < HD; d += 8) {
-            const uint4 kv = *reinterpret_cast<const uint4*>(krow + d);
-            const uint32_t w[4] = {kv.x, kv.y, kv.z, kv.w};
-            float kf[8];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                kf[2 * e] = bf16_lo(w[e]);
-                kf[2 * e + 1] = bf16_hi(w[e]);
-            }
-#pragma unroll
-            for (int i = 0; i < kMaxGroup / 2; ++i) {
-                const int g = hgrp + 2 * i;
-                if (g < G) {
-                    const float4 q0 = *reinterpret_cast<const float4*>(&sq[g][d]);
-                    const float4 q1 = *reinterpret_cast<const float4*>(&sq[g][d + 4]);
-                    sc[i] += q0.x * kf[0] + q0.y * kf[1] + q0.z * kf[2] + q0.w * kf[3] +
-                             q1.x * kf[4] + q1.y * kf[5] + q1.z * kf[6] + q1.w * kf[7];
-                }
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < kMaxGroup / 2; ++i) {
-            const int g = hgrp + 2 * i;
-            if (g < G) sp[g][key] = kpos < it.ctx_len ? sc[i] : -FLT_MAX;
-        }
-        __syncthreads();
-        // online softmax per head: warp w handles heads w, w+4
-        {
-            const int w = tid >> 5, l = tid & 31;
-            for (int g = w; g < G; g += 4) {
-                const float a = sp[g][l], c = sp[g][l + 32];
-                float mx = fmaxf(a, c);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                const float m_old = s_m[g];
-                const float m_new = fmaxf(m_old, mx);
-                const float pa = (b * kBlockTokens + l < it.ctx_len) ? exp2f(a - m_new) : 0.f;
-                const float pc = (b * kBlockTokens + l + 32 < it.ctx_len) ? exp2f(c - m_new) : 0.f;
-                sp[g][l] = pa;
-                sp[g][l + 32] = pc;
-                float sum = pa + pc;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-                if (l == 0) {
-                    const float alpha = exp2f(m_old - m_new);
-                    s_alpha[g] = alpha;
-                    s_l[g] = s_l[g] * alpha + sum;
-                    s_m[g] = m_new;
-                }
-            }
-        }
-        __syncthreads();
-        // P.V
-        {
-            const __nv_bfloat16* vcol = &sv[buf][od];
-#pragma unroll
-            for (int i = 0; i < kMaxGroup; ++i) {
-                const int g = ogrp + kOutPerPass * i;
-                if (g < G) acc[i] *= s_alpha[g];
-            }
-#pragma unroll 4
-            for (int t = 0; t < kBlockTokens; t += 4) {
-                const float v0 = __bfloat162float(vcol[(t + 0) * C::kRow]);
-                const float v1 = __bfloat162float(vcol[(t + 1) * C::kRow]);
-                const float v2 = __bfloat162float(vcol[(t + 2) * C::kRow]);
-                const float v3 = __bfloat162float(vcol[(t + 3) * C::kRow]);
-#pragma unroll
-                for (int i = 0; i < kMaxGroup; ++i) {
-                    const int g = ogrp + kOutPerPass * i;
-                    if (g < G) {
-                        const float4 p4 = *reinterpret_cast<const float4*>(&sp[g][t]);
-                        acc[i] += p4.x * v0 + p4.y * v1 + p4.z * v2 + p4.w * v3;
-                    }
-                }
-            }
-        }
-        __syncthreads();
-    }
-    // partials
-    const size_t row_base = (static_cast<size_t>(blockIdx.x) * s.hq) * gridDim.z;
-#pragma unroll
-    for (int i = 0; i < kMaxGroup; ++i) {
-        const int g = ogrp + kOutPerPass * i;
-        if (g < G) {
-            const int h = kvh * G + g;
-            const size_t slot = row_base + static_cast<size_t>(h) * gridDim.z + split;
-            part_o[slot * HD + od] = acc[i];
-        }
-    }
-    if (tid < G) {
-        const int h = kvh * G + tid;
-        const size_t slot = row_base + static_cast<size_t>(h) * gridDim.z + split;
-        part_ml[slot * 2 + 0] = s_m[tid];
-        part_ml[slot * 2 + 1] = s_l[tid];
-    }
-}
-
-// Merge split partials -> normalised bf16 output.  grid = (n_items, hq), block = HD.
-template <int HD>
-__global__ void decode_combine_kernel(const DecodeItem* __restrict__ items,
-                                      const float* __restrict__ part_o,
-                                      const float* __restrict__ part_ml, int splits,
-                                      __nv_bfloat16* __restrict__ out, int hq) {
-    const int row = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
-    const size_t base = (static_cast<size_t>(row) * hq + h) * splits;
-    float m = -FLT_MAX;
-    for (int sp = 0; sp < splits; ++sp) m = fmaxf(m, part_ml[(base + sp) * 2]);
-    float l = 0.f, o = 0.f;
-    for (int sp = 0; sp < splits; ++sp) {
-        const float ms = part_ml[(base + sp) * 2];
-        const float ls = part_ml[(base + sp) * 2 + 1];
-        if (ls == 0.f) continue;
-        const float w = exp2f(ms - m);
-        l += ls * w;
-        o += part_o[(base + sp) * HD + d] * w;
-    }
-    out[static_cast<size_t>(items[row].q_row) * hq * HD + h * HD + d] = __float2bfloat16_rn(o / l);
-}
-
 // Merge split-KV partials of prefill rows.  grid = (n_items, hkv, 128 rows), block = HD.
 template <int HD>
 __global__ void prefill_combine_kernel(const PrefillItem* __restrict__ items,
@@ -636,45 +391,6 @@ cudaError_t prefill_attention(const CUtensorMap& tmap_q, const CUtensorMap& tmap
         return prefill_launch<64>(tmap_q, tmap_k, tmap_v, items, n_items, max_blocks, splits, tables,
                                   out, part_o, part_ml, s, stream);
     return cudaErrorInvalidValue;
-}
-
-int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits) {
-    const int blocks = (max_ctx + kBlockTokens - 1) / kBlockTokens;
-    const int base = n_items * hkv;
-    int splits = (3 * num_sms + base - 1) / (base > 0 ? base : 1);
-    if (splits > blocks) splits = blocks;
-    if (splits > max_splits) splits = max_splits;
-    if (splits < 1) splits = 1;
-    return splits;
-}
-
-cudaError_t decode_attention(const __nv_bfloat16* q, const __nv_bfloat16* k_pool,
-                             const __nv_bfloat16* v_pool, const DecodeItem* items, int n_items,
-                             int max_ctx, const int32_t* tables, __nv_bfloat16* out,
-                             float* part_o, float* part_ml, int max_splits, int num_sms,
-                             const AttnShape& s, cudaStream_t stream) {
-    if (n_items <= 0) return cudaSuccess;
-    if (s.hq / s.hkv > kMaxGroup) return cudaErrorInvalidValue;
-    const int splits = decode_splits(n_items, s.hkv, max_ctx, num_sms, max_splits);
-    const int blocks = (max_ctx + kBlockTokens - 1) / kBlockTokens;
-    const int bps = (blocks + splits - 1) / splits;
-    dim3 grid(n_items, s.hkv, splits);
-    if (s.hd == 128) {
-        if (cudaError_t e = decode_prepare<128>(); e != cudaSuccess) return e;
-        decode_attention_kernel<128><<<grid, kDThreads, DCfg<128>::kSmem, stream>>>(q, k_pool, v_pool, items,
-                                                                     tables, part_o, part_ml, bps, s);
-        decode_combine_kernel<128><<<dim3(n_items, s.hq), 128, 0, stream>>>(items, part_o, part_ml,
-                                                                          splits, out, s.hq);
-    } else if (s.hd == 64) {
-        if (cudaError_t e = decode_prepare<64>(); e != cudaSuccess) return e;
-        decode_attention_kernel<64><<<grid, kDThreads, DCfg<64>::kSmem, stream>>>(q, k_pool, v_pool, items,
-                                                                    tables, part_o, part_ml, bps, s);
-        decode_combine_kernel<64><<<dim3(n_items, s.hq), 64, 0, stream>>>(items, part_o, part_ml,
-                                                                        splits, out, s.hq);
-    } else {
-        return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
 }
 
 }  // namespace asb

@@ -41,7 +41,7 @@ struct GemmCfg {
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // Apply the epilogue to one output value pair-free path (all modes except SiLU).
 struct Epi {
@@ -119,8 +119,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (elect_one()) {
-            // Streamed operand (weights) is read once per unit: evict-first in L2.
-            const uint64_t pol_stream = policy_evict_first();
+            // swap (decode): each weight tile is read by exactly one CTA -> evict-first; the
+            // tiny activation operand is shared by all -> evict-last.  normal (prefill): a
+            // weight tile is re-read by every M-tile in flight and the activation panel by
+            // every N-tile, so both are kept (evict-last).
+            const uint64_t pol_stream = p.swap ? policy_evict_first() : policy_evict_last();
             const uint64_t pol_keep = policy_evict_last();
             uint32_t stage = 0, phase = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -208,12 +211,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (m < p.tokens) {
                             __nv_bfloat16* o =
                                 p.out + static_cast<size_t>(m) * p.ldo + (n0 >> 1);
+                            if (n0 + 32 <= p.n_out && ((p.ldo & 7) == 0)) {
+                                // 16 outputs = two 16-byte stores
+                                uint32_t pk[8];
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                const float g = __uint_as_float(r[2 * j]);
-                                const float v = __uint_as_float(r[2 * j + 1]);
-                                if (n0 + 2 * j + 1 < p.n_out)
-                                    o[j] = __float2bfloat16_rn(silu(g) * v);
+                                for (int j = 0; j < 8; ++j) {
+                                    const float g0 = __uint_as_float(r[4 * j]), v0 = __uint_as_float(r[4 * j + 1]);
+                                    const float g1 = __uint_as_float(r[4 * j + 2]), v1 = __uint_as_float(r[4 * j + 3]);
+                                    pk[j] = pack_bf16(silu(g0) * v0, silu(g1) * v1);
+                                }
+                                uint4* o4 = reinterpret_cast<uint4*>(o);
+                                o4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                                o4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 16; ++j) {
+                                    const float g = __uint_as_float(r[2 * j]);
+                                    const float v = __uint_as_float(r[2 * j + 1]);
+                                    if (n0 + 2 * j + 1 < p.n_out)
+                                        o[j] = __float2bfloat16_rn(silu(g) * v);
+                                }
                             }
                         }
                     } else {
