@@ -48,10 +48,10 @@ cudaError_t prefill_attention(const CUtensorMap& tmap_q, const CUtensorMap& tmap
                               __nv_bfloat16* out, float* part_o, float* part_ml, const AttnShape& s,
                               cudaStream_t stream);
 
-// Split-K paged decode attention. partial_* workspaces are sized by the caller for
-// n_items * hq * max_splits entries.
-cudaError_t decode_attention(const __nv_bfloat16* q, const __nv_bfloat16* k_pool,
-                             const __nv_bfloat16* v_pool, const DecodeItem* items, int n_items,
+// Split-KV paged decode attention.  tmap_k32 / tmap_v32: the pool maps with 32-row boxes.
+// part_* workspaces are sized by the caller for n_items * hq * max_splits entries.
+cudaError_t decode_attention(const CUtensorMap& tmap_k32, const CUtensorMap& tmap_v32,
+                             const __nv_bfloat16* q, const DecodeItem* items, int n_items,
                              int max_ctx, const int32_t* tables, __nv_bfloat16* out,
                              float* part_o, float* part_ml, int max_splits, int num_sms,
                              const AttnShape& s, cudaStream_t stream);

@@ -1,23 +1,29 @@
-// Paged decode attention (K2 in SURVEY §2.3) — one query token per decode row, all G query
-// heads of one KV head per CTA.  HBM-bound: every context token's K and V row is streamed
-// exactly once per (row, KV head).  Replaces the mu_D term of the reference's
+// Paged decode attention (K2 in SURVEY §2.3) — one query token per decode row, the G query
+// heads of one KV head per CTA.  HBM-bound: each context token's K and V row is streamed
+// from HBM exactly once per (row, KV head).  Replaces the mu_D term of the reference's
 // decode_step_duration_ms (/root/reference/proj/src/executor.cpp:213-215).
 //
 // CTA = 1 producer warp + kWarps consumer warps, split-KV over gridDim.z:
-//   producer   : 1-D bulk copies (cp.async.bulk, evict-first) of contiguous 32-token K and V
-//                sub-blocks ([block][kv_head][64][hd] pool layout) into a kStages-deep smem
-//                ring, completion on mbarriers (expect_tx)
-//   consumers  : each warp owns whole sub-blocks (no CTA-wide barrier per block); lane l owns
-//                head-dim slice [l*DPL, (l+1)*DPL); K slice kept in registers; per head the
-//                32 partial dot products are reduce-scattered across lanes (31 shuffles) so
-//                lane t ends with key t's score; online softmax per warp; P broadcast through
-//                a per-warp smem row; O slice accumulated in registers
-//   epilogue   : warps merge (m, l, O) in smem; CTA writes bf16 output (one split) or fp32
-//                partials merged by decode_combine_kernel.
+//   producer  : TMA (SWIZZLE_128B, evict-first) loads of 32-token K and V sub-blocks straight
+//               from the paged pool into a kStages-deep smem ring, completion on mbarriers
+//   consumers : each warp owns whole sub-blocks (no CTA-wide barrier per block).  The G <= 8
+//               heads are the M rows of a warp-level bf16 tensor-core tile (m16n8k16):
+//                 S = Q . K^T   (B fragments by ldmatrix from the swizzled K tile)
+//                 online softmax on the S fragments (quad shuffles, per-warp m / l)
+//                 O += P . V    (P re-packed from the S fragments in registers, V fragments
+//                                by ldmatrix.trans)
+//               ~230 instructions per 32-key sub-block for all heads at once, so the kernel
+//               stays bandwidth-bound.  (tcgen05 needs M >= 64 — >= 8x wasted rows for
+//               G <= 8 — and a TMEM round trip per block; a register-resident warp MMA is
+//               the better fit for this memory-bound shape.)
+//   epilogue  : warps merge (m, l, O) through smem; the CTA writes bf16 output (one split)
+//               or fp32 partials merged by decode_combine_kernel.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "attn.h"
 #include "sm100.cuh"
@@ -26,66 +32,87 @@ namespace asb {
 
 namespace {
 
-constexpr int kSub = 32;    // tokens per streamed sub-block (half a KV block)
-constexpr int kWarps = 4;   // consumer warps per CTA
+constexpr int kSub = 32;   // tokens per streamed sub-block (half a KV block)
+constexpr int kWarps = 4;  // consumer warps per CTA (two CTAs per SM, see DC::kStages)
 constexpr int kThreadsD = (kWarps + 1) * 32;
 
 template <int HD>
 struct DC {
-    static constexpr int kDpl = HD / 32;                  // head dims per lane
-    static constexpr int kSubBytes = kSub * HD * 2;       // one K (or V) sub-block
-    static constexpr int kStages = HD == 128 ? 5 : 10;    // 80 KB ring -> 2 CTAs / SM
-    static constexpr int kRing = kStages * 2 * kSubBytes;
+    static constexpr int kHalves = HD / 64;                // 64-column SW128 boxes per row
+    static constexpr int kTile = kSub * HD * 2;            // one K (or V) sub-block, bytes
+    static constexpr int kStage = 2 * kTile;
+    // One stage per consumer warp (HD=128: 64 KB ring + 16 KB merge) or two (HD=64): two
+    // CTAs per SM, i.e. 8 consumer warps and 128 KB of K/V in flight per SM.  Measured best
+    // of the (warps, stages) sweep in profiles/r1_decode_attn_sweep.txt.
+    static constexpr int kStages = HD == 128 ? 4 : 8;
+    static constexpr int kRing = kStages * kStage;
 };
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-        : "memory");
-}
 
 __device__ __forceinline__ void named_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// lane l returns sum over lanes of v[l] (reduce-scatter of 32 partials)
-__device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int k = 0; k < o; ++k) {
-            const float send = up ? v[k] : v[k + o];
-            const float keep = up ? v[k + o] : v[k];
-            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-    }
-    return v[0];
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+// D = A (16x16 bf16, row) * B (16x8 bf16, col) + D, fp32 accumulate
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-template <int HD, int G>
+// byte offset of 16-byte chunk `c` (0..HD/8-1) of row `r` in a [rows][HD] tile stored as
+// HD/64 SWIZZLE_128B boxes of [kSub rows][64 cols]
+template <int HD>
+__device__ __forceinline__ uint32_t sw_off(int r, int c) {
+    const int box = c >> 3, cc = c & 7;
+    return box * (kSub * 128) + r * 128 + ((cc ^ (r & 7)) << 4);
+}
+
+// Stage of item i.  Item i is consumed by warp i % W; giving every warp its own S / W stages
+// (visited in order) means each mbarrier has exactly one waiter that waits its phases
+// strictly in sequence — with round-robin consumers sharing a ring, a fast warp could wait
+// for phase k+2 of a stage while phase k+1 is still pending, and the parity-based wait would
+// alias and return early.
+__device__ __forceinline__ int stage_of(int i, int W, int S) { return (i % W) + W * ((i / W) % (S / W)); }
+
+template <int HD>
 __global__ void __launch_bounds__(kThreadsD, 2)
-    decode_attn_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_pool,
-                       const __nv_bfloat16* __restrict__ v_pool, const DecodeItem* __restrict__ items,
+    decode_attn_kernel(const __grid_constant__ CUtensorMap tmap_k,
+                       const __grid_constant__ CUtensorMap tmap_v,
+                       const __nv_bfloat16* __restrict__ q, const DecodeItem* __restrict__ items,
                        const int32_t* __restrict__ tables, __nv_bfloat16* __restrict__ out,
                        float* __restrict__ part_o, float* __restrict__ part_ml, int subs_per_split,
-                       AttnShape s) {
+                       int n_stages, AttnShape s) {
     using C = DC<HD>;
-    constexpr int DPL = C::kDpl;
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* ring = smem;                                                // [stage][K|V][sub]
-    float* pbuf = reinterpret_cast<float*>(smem + C::kRing);             // [warp][32]
-    float* qs = pbuf + kWarps * 32;                                      // [G][HD] scaled q
-    float* accs = qs + G * HD;                                           // [warp][G][HD]
-    float* mls = accs + kWarps * G * HD;                                 // [warp][G][2]
-    uint64_t* full = reinterpret_cast<uint64_t*>(mls + kWarps * G * 2 + 2);
-    uint64_t* empty = full + C::kStages;
+    constexpr int NT = HD / 8;  // O n-tiles (8 dims each)
+    const int kWarpsR = blockDim.x / 32 - 1;  // consumer warps
+    const int kStagesR = n_stages;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+    uint8_t* ring = smem;
+    float* mrg = reinterpret_cast<float*>(smem + kStagesR * C::kStage);  // [warp][8][HD]
+    float* mls = mrg + kWarpsR * 8 * HD;                                 // [warp][8][2]
+    uint64_t* full = reinterpret_cast<uint64_t*>(mls + kWarpsR * 16);
+    uint64_t* empty = full + kStagesR;
 
     const DecodeItem it = items[blockIdx.x];
     const int kvh = blockIdx.y;
+    const int G = s.hq / s.hkv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_sub = (it.ctx_len + kSub - 1) / kSub;
     const int s0 = blockIdx.z * subs_per_split;
@@ -93,163 +120,169 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     const int32_t* table = tables + it.table_off;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < C::kStages; ++i) {
+        tma_prefetch_desc(&tmap_k);
+        tma_prefetch_desc(&tmap_v);
+        for (int i = 0; i < kStagesR; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
         }
         fence_barrier_init();
     }
-    for (int e = threadIdx.x; e < G * HD; e += blockDim.x)
-        qs[e] = __bfloat162float(q[(size_t)it.q_row * s.hq * HD + kvh * G * HD + e]) * s.scale_log2;
-    for (int e = threadIdx.x; e < kWarps * G * HD; e += blockDim.x) accs[e] = 0.f;
-    for (int e = threadIdx.x; e < kWarps * G; e += blockDim.x) {
-        mls[2 * e] = -FLT_MAX;
-        mls[2 * e + 1] = 0.f;
-    }
     __syncthreads();
 
-    if (warp == kWarps) {
+    if (warp == kWarpsR) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             for (int i = 0; i < n_local; ++i) {
-                const int st = i % C::kStages;
-                mbar_wait(&empty[st], ((i / C::kStages) & 1) ^ 1);
-                mbar_expect_tx(&full[st], 2 * C::kSubBytes);
+                const int st = stage_of(i, kWarpsR, kStagesR);
+                mbar_wait(&empty[st], ((i / kStagesR) & 1) ^ 1);
+                mbar_expect_tx(&full[st], C::kStage);
                 const int j = s0 + i;
                 const int blk = table[j >> 1];
-                const size_t off =
-                    ((((size_t)s.layer * s.num_blocks + blk) * s.hkv + kvh) * kBlockTokens + (j & 1) * kSub) * HD;
-                uint8_t* dst = ring + (size_t)st * 2 * C::kSubBytes;
-                bulk_g2s(dst, k_pool + off, C::kSubBytes, &full[st], pol);
-                bulk_g2s(dst + C::kSubBytes, v_pool + off, C::kSubBytes, &full[st], pol);
+                const int row = ((s.layer * s.num_blocks + blk) * s.hkv + kvh) * kBlockTokens + (j & 1) * kSub;
+                uint8_t* kd = ring + st * C::kStage;
+                uint8_t* vd = kd + C::kTile;
+#pragma unroll
+                for (int h = 0; h < C::kHalves; ++h) {
+                    tma_load_2d_hint(kd + h * (kSub * 128), &tmap_k, &full[st], h * 64, row, pol);
+                    tma_load_2d_hint(vd + h * (kSub * 128), &tmap_v, &full[st], h * 64, row, pol);
+                }
             }
         }
         return;
     }
 
     // ---------------------------------------------------------------- consumers
-    // per-head state (q slice, O slice, m, l) lives in smem so the head loop stays rolled and
-    // register use is independent of G
-    float* prow = pbuf + warp * 32;
-    float* wacc = accs + warp * G * HD;
-    float* wml = mls + warp * G * 2;
-    for (int i = warp; i < n_local; i += kWarps) {
-        const int st = i % C::kStages;
-        mbar_wait(&full[st], (i / C::kStages) & 1);
-        const uint8_t* kt = ring + (size_t)st * 2 * C::kSubBytes;
-        const uint8_t* vt = kt + C::kSubBytes;
+    const int g = lane >> 2, t = lane & 3;  // fragment row / column-pair owner
+    // Q A-fragments (rows = heads): (row g, k 2t..2t+1) and (row g, k 2t+8..2t+9); the
+    // fragment registers of rows g+8 and of rows >= G are zero
+    uint32_t qa[HD / 16][2];
+    {
+        const __nv_bfloat16* qrow = q + (size_t)it.q_row * s.hq * HD + (size_t)(kvh * G + g) * HD;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+            if (g < G) {
+                qa[kk][0] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t);
+                qa[kk][1] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t + 8);
+            } else {
+                qa[kk][0] = qa[kk][1] = 0u;
+            }
+        }
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_run = -FLT_MAX, l_run = 0.f;
+
+    for (int i = warp; i < n_local; i += kWarpsR) {
+        const int st = stage_of(i, kWarpsR, kStagesR);
+        mbar_wait(&full[st], (i / kStagesR) & 1);
+        const uint32_t kt = smem_u32(ring + st * C::kStage);
+        const uint32_t vt = kt + C::kTile;
+        // ---- S = Q K^T : 4 n-tiles of 8 keys
+        float sacc[4][4];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+#pragma unroll
+            for (int np = 0; np < 2; ++np) {  // pairs of key n-tiles
+                // matrices: (ntile 2np, k lo), (2np, k hi), (2np+1, k lo), (2np+1, k hi)
+                const int mi = lane >> 3;
+                const int key = (2 * np + (mi >> 1)) * 8 + (lane & 7);
+                const int chunk = 2 * kk + (mi & 1);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(kt + sw_off<HD>(key, chunk), b0, b1, b2, b3);
+                mma16816(sacc[2 * np], qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
+                mma16816(sacc[2 * np + 1], qa[kk][0], 0u, qa[kk][1], 0u, b2, b3);
+            }
+        }
+        // ---- online softmax on row g (keys 8n + 2t + {0,1})
         const int kbase = (s0 + i) * kSub;
-        const bool valid = kbase + lane < it.ctx_len;
-        // K slice of all 32 keys in registers, packed bf16x2 (lane's DPL dims of each row)
-        uint32_t kw[kSub][DPL / 2];
+        float mx = m_run;
 #pragma unroll
-        for (int t = 0; t < kSub; ++t) {
-            if constexpr (DPL == 4) {
-                const uint2 w = *reinterpret_cast<const uint2*>(kt + (t * HD + lane * 4) * 2);
-                kw[t][0] = w.x;
-                kw[t][1] = w.y;
-            } else {
-                kw[t][0] = *reinterpret_cast<const uint32_t*>(kt + (t * HD + lane * 2) * 2);
+        for (int n = 0; n < 4; ++n)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const bool ok = kbase + 8 * n + 2 * t + e < it.ctx_len;
+                sacc[n][e] = ok ? sacc[n][e] * s.scale_log2 : -FLT_MAX;
+                mx = fmaxf(mx, sacc[n][e]);
+            }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float alpha = exp2f(m_run - mx);
+        float psum = 0.f;
+        uint32_t pa[2][2];  // P A-fragments for the two 16-key k-steps (row g)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+            const float p0 = sacc[n][0] == -FLT_MAX ? 0.f : exp2f(sacc[n][0] - mx);
+            const float p1 = sacc[n][1] == -FLT_MAX ? 0.f : exp2f(sacc[n][1] - mx);
+            const uint32_t pk = pack_bf16(p0, p1);
+            psum += bf16_lo(pk) + bf16_hi(pk);  // sum what P.V will actually use
+            pa[n >> 1][n & 1] = pk;
+        }
+        psum += __shfl_xor_sync(0xffffffffu, psum, 1);
+        psum += __shfl_xor_sync(0xffffffffu, psum, 2);
+        l_run = l_run * alpha + psum;
+        m_run = mx;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            o[n][0] *= alpha;
+            o[n][1] *= alpha;
+        }
+        // ---- O += P V : 2 k-steps of 16 keys x NT n-tiles of 8 dims
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+#pragma unroll
+            for (int dp = 0; dp < NT / 2; ++dp) {  // pairs of dim n-tiles
+                const int mi = lane >> 3;
+                const int key = ks * 16 + (mi & 1) * 8 + (lane & 7);
+                const int chunk = 2 * dp + (mi >> 1);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(vt + sw_off<HD>(key, chunk), b0, b1, b2, b3);
+                mma16816(o[2 * dp], pa[ks][0], 0u, pa[ks][1], 0u, b0, b1);
+                mma16816(o[2 * dp + 1], pa[ks][0], 0u, pa[ks][1], 0u, b2, b3);
             }
         }
-#pragma unroll 1
-        for (int g = 0; g < G; ++g) {
-            float qv[DPL], acc[DPL];
-            if constexpr (DPL == 4) {
-                const float4 a = *reinterpret_cast<const float4*>(qs + g * HD + lane * 4);
-                qv[0] = a.x; qv[1] = a.y; qv[2] = a.z; qv[3] = a.w;
-                const float4 c = *reinterpret_cast<const float4*>(wacc + g * HD + lane * 4);
-                acc[0] = c.x; acc[1] = c.y; acc[2] = c.z; acc[3] = c.w;
-            } else {
-                const float2 a = *reinterpret_cast<const float2*>(qs + g * HD + lane * 2);
-                qv[0] = a.x; qv[1] = a.y;
-                const float2 c = *reinterpret_cast<const float2*>(wacc + g * HD + lane * 2);
-                acc[0] = c.x; acc[1] = c.y;
-            }
-            float part[kSub];
-#pragma unroll
-            for (int t = 0; t < kSub; ++t) {
-                float a = 0.f;
-#pragma unroll
-                for (int d2 = 0; d2 < DPL / 2; ++d2) {
-                    a = fmaf(qv[2 * d2], bf16_lo(kw[t][d2]), a);
-                    a = fmaf(qv[2 * d2 + 1], bf16_hi(kw[t][d2]), a);
-                }
-                part[t] = a;
-            }
-            const float red = reduce_scatter32(part, lane);  // all lanes take part in the shuffles
-            const float sc = valid ? red : -FLT_MAX;
-            float mx = sc;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            const float m_old = wml[2 * g];
-            const float m_new = fmaxf(m_old, mx);
-            const float p = valid ? exp2f(sc - m_new) : 0.f;
-            float sum = p;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            const float alpha = exp2f(m_old - m_new);
-            prow[lane] = p;
-            __syncwarp();
-#pragma unroll
-            for (int d = 0; d < DPL; ++d) acc[d] *= alpha;
-#pragma unroll
-            for (int t = 0; t < kSub; t += 4) {
-                const float4 p4 = *reinterpret_cast<const float4*>(prow + t);
-                const float pp[4] = {p4.x, p4.y, p4.z, p4.w};
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if constexpr (DPL == 4) {
-                        const uint2 w = *reinterpret_cast<const uint2*>(vt + ((t + u) * HD + lane * 4) * 2);
-                        acc[0] = fmaf(pp[u], bf16_lo(w.x), acc[0]);
-                        acc[1] = fmaf(pp[u], bf16_hi(w.x), acc[1]);
-                        acc[2] = fmaf(pp[u], bf16_lo(w.y), acc[2]);
-                        acc[3] = fmaf(pp[u], bf16_hi(w.y), acc[3]);
-                    } else {
-                        const uint32_t w = *reinterpret_cast<const uint32_t*>(vt + ((t + u) * HD + lane * 2) * 2);
-                        acc[0] = fmaf(pp[u], bf16_lo(w), acc[0]);
-                        acc[1] = fmaf(pp[u], bf16_hi(w), acc[1]);
-                    }
-                }
-            }
-            if constexpr (DPL == 4) {
-                *reinterpret_cast<float4*>(wacc + g * HD + lane * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            } else {
-                *reinterpret_cast<float2*>(wacc + g * HD + lane * 2) = make_float2(acc[0], acc[1]);
-            }
-            __syncwarp();  // prow / wml reads of this head are done before they are overwritten
-            if (lane == 0) {
-                wml[2 * g] = m_new;
-                wml[2 * g + 1] = wml[2 * g + 1] * alpha + sum;
-            }
-            __syncwarp();
-        }
+        __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
     }
 
     // ---------------------------------------------------------------- merge warps
-    named_sync(1, kWarps * 32);
+    float* mw = mrg + warp * 8 * HD;
+    if (g < G) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            mw[g * HD + n * 8 + 2 * t] = o[n][0];
+            mw[g * HD + n * 8 + 2 * t + 1] = o[n][1];
+        }
+        if (t == 0) {
+            mls[(warp * 8 + g) * 2] = m_run;
+            mls[(warp * 8 + g) * 2 + 1] = l_run;
+        }
+    }
+    named_sync(1, kWarpsR * 32);
     const bool single = gridDim.z == 1;
-    for (int e = threadIdx.x; e < G * HD; e += kWarps * 32) {
-        const int g = e / HD, d = e % HD;
+    for (int e = threadIdx.x; e < G * HD; e += kWarpsR * 32) {
+        const int h = e / HD, d = e % HD;
         float M = -FLT_MAX;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) M = fmaxf(M, mls[(w * G + g) * 2]);
+        for (int w = 0; w < kWarpsR; ++w) M = fmaxf(M, mls[(w * 8 + h) * 2]);
         float L = 0.f, O = 0.f;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            const float lw = mls[(w * G + g) * 2 + 1];
+        for (int w = 0; w < kWarpsR; ++w) {
+            const float lw = mls[(w * 8 + h) * 2 + 1];
             if (lw == 0.f) continue;
-            const float f = exp2f(mls[(w * G + g) * 2] - M);
+            const float f = exp2f(mls[(w * 8 + h) * 2] - M);
             L += lw * f;
-            O += accs[(w * G + g) * HD + d] * f;
+            O += mrg[(w * 8 + h) * HD + d] * f;
         }
-        const int h = kvh * G + g;
+        const int hh = kvh * G + h;
         if (single) {
-            out[(size_t)it.q_row * s.hq * HD + h * HD + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+            out[(size_t)it.q_row * s.hq * HD + hh * HD + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
         } else {
-            const size_t slot = ((size_t)blockIdx.x * s.hq + h) * gridDim.z + blockIdx.z;
+            const size_t slot = ((size_t)blockIdx.x * s.hq + hh) * gridDim.z + blockIdx.z;
             part_o[slot * HD + d] = O;
             if (d == 0) {
                 part_ml[slot * 2 + 0] = M;
@@ -280,72 +313,58 @@ __global__ void decode_combine_kernel(const DecodeItem* __restrict__ items,
     out[(size_t)items[row].q_row * hq * HD + h * HD + d] = __float2bfloat16_rn(O / L);
 }
 
-template <int HD, int G>
-cudaError_t launch_g(const __nv_bfloat16* q, const __nv_bfloat16* kp, const __nv_bfloat16* vp,
-                     const DecodeItem* items, int n_items, int splits, int sps, const int32_t* tables,
-                     __nv_bfloat16* out, float* po, float* pml, const AttnShape& s, cudaStream_t st) {
+template <int HD>
+cudaError_t launch_hd(const CUtensorMap& tk, const CUtensorMap& tv, const __nv_bfloat16* q,
+                      const DecodeItem* items, int n_items, int splits, int sps, const int32_t* tables,
+                      __nv_bfloat16* out, float* po, float* pml, const AttnShape& s, cudaStream_t st) {
     using C = DC<HD>;
-    constexpr int smem = C::kRing + kWarps * 32 * 4 + G * HD * 4 + kWarps * G * HD * 4 +
-                         (kWarps * G * 2 + 2) * 4 + 2 * C::kStages * 8;
+    static const int warps = std::getenv("ASB_DECODE_WARPS") ? std::atoi(std::getenv("ASB_DECODE_WARPS")) : kWarps;
+    static const int stages0 = std::getenv("ASB_DECODE_STAGES") ? std::atoi(std::getenv("ASB_DECODE_STAGES")) : C::kStages;
+    static const int stages = std::max(warps, (stages0 / warps) * warps);  // multiple of warps
+    const int smem = stages * C::kStage + warps * 8 * HD * 4 + warps * 16 * 4 + 2 * stages * 8 + 1024;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD, G>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     dim3 grid(n_items, s.hkv, splits);
-    decode_attn_kernel<HD, G><<<grid, kThreadsD, smem, st>>>(q, kp, vp, items, tables, out, po, pml, sps, s);
+    decode_attn_kernel<HD><<<grid, (warps + 1) * 32, smem, st>>>(tk, tv, q, items, tables, out, po, pml, sps,
+                                                               stages, s);
     if (splits > 1)
         decode_combine_kernel<HD><<<dim3(n_items, s.hq), HD, 0, st>>>(items, po, pml, splits, out, s.hq);
     return cudaGetLastError();
 }
 
-template <int HD>
-cudaError_t launch_hd(int G, const __nv_bfloat16* q, const __nv_bfloat16* kp, const __nv_bfloat16* vp,
-                      const DecodeItem* items, int n_items, int splits, int sps, const int32_t* tables,
-                      __nv_bfloat16* out, float* po, float* pml, const AttnShape& s, cudaStream_t st) {
-    switch (G) {
-    case 1: return launch_g<HD, 1>(q, kp, vp, items, n_items, splits, sps, tables, out, po, pml, s, st);
-    case 2: return launch_g<HD, 2>(q, kp, vp, items, n_items, splits, sps, tables, out, po, pml, s, st);
-    case 3: return launch_g<HD, 3>(q, kp, vp, items, n_items, splits, sps, tables, out, po, pml, s, st);
-    case 4: return launch_g<HD, 4>(q, kp, vp, items, n_items, splits, sps, tables, out, po, pml, s, st);
-    case 5: return launch_g<HD, 5>(q, kp, vp, items, n_items, splits, sps, tables, out, po, pml, s, st);
-    case 6: return launch_g<HD, 6>(q, kp, vp, items, n_items, splits, sps, tables, out, po, pml, s, st);
-    case 7: return launch_g<HD, 7>(q, kp, vp, items, n_items, splits, sps, tables, out, po, pml, s, st);
-    case 8: return launch_g<HD, 8>(q, kp, vp, items, n_items, splits, sps, tables, out, po, pml, s, st);
-    default: return cudaErrorInvalidValue;
-    }
-}
-
 }  // namespace
 
 int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits) {
-    // aim for ~4 resident CTAs per SM-pair worth of work, >= 2 sub-blocks per consumer warp
+    // ~2 waves of one-CTA-per-SM work, >= 2 sub-blocks per consumer warp
     const int subs = (max_ctx + kSub - 1) / kSub;
     const int base = n_items * hkv;
-    int splits = (4 * num_sms + base - 1) / std::max(base, 1);
+    int splits = (2 * num_sms + base - 1) / std::max(base, 1);
     splits = std::min(splits, std::max(1, subs / (2 * kWarps)));
     splits = std::min(splits, max_splits);
     return std::max(splits, 1);
 }
 
-cudaError_t decode_attention(const __nv_bfloat16* q, const __nv_bfloat16* k_pool,
-                             const __nv_bfloat16* v_pool, const DecodeItem* items, int n_items,
+cudaError_t decode_attention(const CUtensorMap& tmap_k32, const CUtensorMap& tmap_v32,
+                             const __nv_bfloat16* q, const DecodeItem* items, int n_items,
                              int max_ctx, const int32_t* tables, __nv_bfloat16* out,
                              float* part_o, float* part_ml, int max_splits, int num_sms,
                              const AttnShape& s, cudaStream_t stream) {
     if (n_items <= 0) return cudaSuccess;
-    const int G = s.hq / s.hkv;
+    if (s.hq / s.hkv > 8) return cudaErrorInvalidValue;
     const int splits0 = decode_splits(n_items, s.hkv, max_ctx, num_sms, max_splits);
     const int subs = (max_ctx + kSub - 1) / kSub;
     const int sps = (subs + splits0 - 1) / splits0;
     const int splits = (subs + sps - 1) / sps;
     if (s.hd == 128)
-        return launch_hd<128>(G, q, k_pool, v_pool, items, n_items, splits, sps, tables, out, part_o,
+        return launch_hd<128>(tmap_k32, tmap_v32, q, items, n_items, splits, sps, tables, out, part_o,
                               part_ml, s, stream);
     if (s.hd == 64)
-        return launch_hd<64>(G, q, k_pool, v_pool, items, n_items, splits, sps, tables, out, part_o,
+        return launch_hd<64>(tmap_k32, tmap_v32, q, items, n_items, splits, sps, tables, out, part_o,
                              part_ml, s, stream);
     return cudaErrorInvalidValue;
 }

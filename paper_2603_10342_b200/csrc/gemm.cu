@@ -20,6 +20,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "gemm.h"
 #include "sm100.cuh"
 
@@ -72,6 +74,48 @@ struct Epi {
     }
 };
 
+// Work decomposition shared by the producer, MMA and epilogue roles.
+//  classic : units (tile, split) strided over the persistent grid
+//  stream-K: CTA b owns the contiguous range [b*W/grid, (b+1)*W/grid) of the flattened
+//            (tile, k-block) space (W = tiles * k_blocks), so every CTA streams the same
+//            number of k-blocks; tile boundaries inside a range flush through fp32 atomics.
+struct Work {
+    int tiles_m, k_blocks, units, splits, kbps, streamk, u;
+    long long pos, hi;
+    __device__ void init(const GemmParams& p, int tm_, int tn_, int kb) {
+        tiles_m = tm_;
+        k_blocks = kb;
+        splits = p.splits;
+        kbps = p.kb_per_split;
+        streamk = p.streamk;
+        units = tm_ * tn_ * p.splits;
+        u = blockIdx.x;
+        const long long total = static_cast<long long>(tm_) * tn_ * kb;
+        pos = total * blockIdx.x / gridDim.x;
+        hi = total * (blockIdx.x + 1) / gridDim.x;
+    }
+    __device__ bool next(int& tm, int& tn, int& kb0, int& kb1) {
+        int tile;
+        if (streamk) {
+            if (pos >= hi) return false;
+            tile = static_cast<int>(pos / k_blocks);
+            kb0 = static_cast<int>(pos % k_blocks);
+            kb1 = static_cast<int>(min(static_cast<long long>(k_blocks), kb0 + (hi - pos)));
+            pos += kb1 - kb0;
+        } else {
+            if (u >= units) return false;
+            const int split = u % splits;
+            tile = u / splits;
+            kb0 = split * kbps;
+            kb1 = min(k_blocks, kb0 + kbps);
+            u += gridDim.x;
+        }
+        tm = tile % tiles_m;
+        tn = tile / tiles_m;
+        return true;
+    }
+};
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -115,7 +159,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tiles_m = (p.M + BM - 1) / BM;
     const int tiles_n = (p.N + BN - 1) / BN;
     const int k_blocks = (p.K + BK - 1) / BK;
-    const int units = tiles_m * tiles_n * p.splits;
 
     if (warp == 0) {
         if (elect_one()) {
@@ -126,13 +169,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol_stream = p.swap ? policy_evict_first() : policy_evict_last();
             const uint64_t pol_keep = policy_evict_last();
             uint32_t stage = 0, phase = 0;
-            for (int u = blockIdx.x; u < units; u += gridDim.x) {
-                const int split = u % p.splits;
-                const int tile = u / p.splits;
-                const int tm = tile % tiles_m;
-                const int tn = tile / tiles_m;
-                const int kb0 = split * p.kb_per_split;
-                const int kb1 = min(k_blocks, kb0 + p.kb_per_split);
+            Work w;
+            w.init(p, tiles_m, tiles_n, k_blocks);
+            int tm, tn, kb0, kb1;
+            while (w.next(tm, tn, kb0, kb1)) {
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     mbar_expect_tx(&full_bar[stage], C::kStageBytes);
@@ -151,10 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
         uint32_t stage = 0, phase = 0;
         uint32_t local = 0;
-        for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
-            const int split = u % p.splits;
-            const int kb0 = split * p.kb_per_split;
-            const int kb1 = min(k_blocks, kb0 + p.kb_per_split);
+        Work w;
+        w.init(p, tiles_m, tiles_n, k_blocks);
+        int tm, tn, kb0, kb1;
+        for (; w.next(tm, tn, kb0, kb1); ++local) {
             const uint32_t ab = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tempty_bar[ab], acc_phase ^ 1);
@@ -189,10 +229,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t row_in_tile = quarter * 32 + lane;
         Epi epi{p};
         uint32_t local = 0;
-        for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
-            const int tile = u / p.splits;
-            const int tm = tile % tiles_m;
-            const int tn = tile / tiles_m;
+        Work w;
+        w.init(p, tiles_m, tiles_n, k_blocks);
+        int tm, tn, kb0, kb1;
+        for (; w.next(tm, tn, kb0, kb1); ++local) {
             const uint32_t ab = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tfull_bar[ab], acc_phase);
@@ -370,8 +410,14 @@ cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const GemmPa
         attr_set = true;
     }
     const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
-    const int units = tiles * p.splits;
-    const int grid = units < num_sms ? units : num_sms;
+    int grid;
+    if (p.streamk) {
+        const long long work = static_cast<long long>(tiles) * ((p.K + BK - 1) / BK);
+        grid = static_cast<int>(std::min<long long>(num_sms, std::max<long long>(1, work / 4)));
+    } else {
+        const int units = tiles * p.splits;
+        grid = units < num_sms ? units : num_sms;
+    }
     gemm_tn_kernel<BN><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
     return cudaGetLastError();
 }
@@ -388,7 +434,10 @@ int gemm_pick_bn(int n) {
 cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int bn,
                         int num_sms, cudaStream_t stream) {
     const int k_blocks = (p.K + BK - 1) / BK;
-    if (p.splits <= 1) {
+    if (p.streamk) {
+        p.splits = 1;
+        p.kb_per_split = k_blocks;
+    } else if (p.splits <= 1) {
         p.splits = 1;
         p.kb_per_split = k_blocks;
     } else {
@@ -396,7 +445,7 @@ cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams
         p.splits = (k_blocks + p.kb_per_split - 1) / p.kb_per_split;
     }
     GemmParams kp = p;
-    const bool split = p.splits > 1;
+    const bool split = p.splits > 1 || p.streamk;
     if (split) kp.epi = EPI_ATOMIC;
     cudaError_t e;
     switch (bn) {

@@ -18,6 +18,7 @@ struct GemmParams {
     int tokens, n_out;    // logical view: Y[tokens][n_out]
     int swap;             // 0: A = X, B = W.  1: A = W, B = X (Y = D^T)
     int splits, kb_per_split;
+    int streamk;          // 1: balanced stream-K over (tile, k-block); epilogue via ws atomics
     int epi;
     __nv_bfloat16* out;   // Y (bf16), row stride ldo
     float* out_f32;       // Y (fp32), row stride ldo

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -218,7 +219,8 @@ struct asb_kv {
     asb_model* m = nullptr;
     int nb = 0;
     __nv_bfloat16 *k_pool = nullptr, *v_pool = nullptr;
-    CUtensorMap tk, tv;
+    CUtensorMap tk, tv;      // box 64 rows (prefill attention)
+    CUtensorMap tk32, tv32;  // box 32 rows (decode attention sub-blocks)
     std::vector<int> free_list;  // LIFO: back() is handed out next
     struct Sess {
         std::vector<int32_t> blocks;
@@ -380,6 +382,9 @@ void linear(asb_lane* L, const CUtensorMap* xmaps, const Weight& w, int T, int e
         if (force_splits <= 0) splits = std::min(splits, std::max(1, kb / 4));
         if (epi == EPI_F32 && force_splits <= 0) splits = 1;
         p.splits = splits;
+        // balanced stream-K whenever whole tiles would leave a ragged last wave (the fp32
+        // workspace holds <= 256 token rows; the LM head writes fp32 logits directly)
+        p.streamk = (force_splits <= 0 && epi != EPI_F32 && (tiles % num_sms) != 0 && tiles < 8 * num_sms) ? 1 : 0;
         e = gemm_launch(w.map_a128, xmaps[swap_map_index(bn)], p, bn, num_sms, L->stream);
     } else {
         p.swap = 0;
@@ -563,7 +568,9 @@ asb_status asb_kv_create(asb_model* m, int num_blocks, asb_kv** out) {
         const long rows = long(s.layers) * num_blocks * s.hkv * kBlockTokens;
         if (rows >= (1l << 31)) fail(ASB_ERR_VALIDATION, "KV pool too large for 32-bit TMA rows");
         if (!make_tmap_bf16(&kv->tk, kv->k_pool, int(rows), s.hd, s.hd, kBlockTokens) ||
-            !make_tmap_bf16(&kv->tv, kv->v_pool, int(rows), s.hd, s.hd, kBlockTokens))
+            !make_tmap_bf16(&kv->tv, kv->v_pool, int(rows), s.hd, s.hd, kBlockTokens) ||
+            !make_tmap_bf16(&kv->tk32, kv->k_pool, int(rows), s.hd, s.hd, 32) ||
+            !make_tmap_bf16(&kv->tv32, kv->v_pool, int(rows), s.hd, s.hd, 32))
             fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for the KV pool");
         kv->free_list.reserve(num_blocks);
         for (int b = num_blocks - 1; b >= 0; --b) kv->free_list.push_back(b);
@@ -688,6 +695,7 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->m = m;
         const ModelSpec& s = m->spec;
         L->max_T = max_tokens;
+        if (const char* e = std::getenv("ASB_DECODE_MAX_SPLITS")) L->max_splits = std::max(1, std::atoi(e));
         L->max_segs = std::min(max_segments, max_tokens);
         L->max_tbl = L->max_segs * ((m->max_ctx + kBlockTokens - 1) / kBlockTokens);
         L->max_pitems = max_tokens / prefill_tokens_per_tile(s.hq, s.hkv) + L->max_segs;
@@ -894,7 +902,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                        "rope_append");
             if (!ditems.empty())
                 L->timed(ASB_STAT_DECODE_ATTN, dattn_bytes, [&] {
-                    cuda_check(decode_attention(L->q, kv->k_pool, kv->v_pool, d_ditems, int(ditems.size()),
+                    cuda_check(decode_attention(kv->tk32, kv->tv32, L->q, d_ditems, int(ditems.size()),
                                                 max_ctx, d_tbl, L->attn, L->part_o, L->part_ml,
                                                 L->max_splits, L->n_sms(), as, st),
                                "decode attention");

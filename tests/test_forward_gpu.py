@@ -64,16 +64,25 @@ def _kv_check(kv, sess_dev, osess, positions, layers, per_layer):
                     assert np.abs(da - db).mean() <= 0.01 * scale, f"pos {p} layer {l}: mean dev"
 
 
+# head_dim 128, GQA group 3 (Llama-3.2-3B head layout) at tiny width, with contexts long
+# enough that decode attention splits the KV range across CTAs
+HD128 = dict(layers=2, d=256, hq=6, hkv=2, hd=128, ffn=512, vocab=4096, tied=1, qkv_bias=0,
+             theta=500000.0, eps=1e-5)
+HD128_JSON = ('{"name":"hd128","layers":2,"d_model":256,"n_heads":6,"n_kv_heads":2,"head_dim":128,'
+              '"ffn":512,"vocab":4096,"tied":true,"qkv_bias":false,"rope_theta":500000.0,"rms_eps":1e-5}')
+
+
 @pytest.mark.parametrize("spec,prompt_lens,steps", [
     ("tiny", (200, 70), 12),
     ("qwen2.5-0.5b", (130, 64), 6),
+    ("hd128", (2500, 1300), 6),
 ])
 def test_forward_matches_oracle(spec, prompt_lens, steps):
     seed = 13
-    m = Model(spec, seed=seed, max_context=4096)
+    m = Model(HD128_JSON if spec == "hd128" else spec, seed=seed, max_context=4096)
     kv = KvPool(m, num_blocks=128)
-    lane = Lane(m, max_tokens=1024, max_segments=32)
-    om = OracleModel(spec, seed=seed, max_ctx=4096)
+    lane = Lane(m, max_tokens=4096, max_segments=32)
+    om = OracleModel(HD128 if spec == "hd128" else spec, seed=seed, max_ctx=4096)
     V = m.vocab
     osess = [om.session() for _ in prompt_lens]
     stats = {"match": 0, "near_tie": 0}
