@@ -165,6 +165,9 @@ asb_status asb_slots_sm_counts(const asb_slots* s, int decode_level, int* decode
 /* --- debug / test hooks (used by tests/, not by the engine) --------------------------------*/
 /* Y[tokens][n_out] = X[tokens][k] . W[n_out][k]^T on device pointers; epi: 0 bf16(+bias),
  * 1 +resid, 2 silu-mul (interleaved rows), 3 fp32.  force_path: -1 auto, 0 normal, 1 swap. */
+/* ASB_GEMM_TIMELINE=1: per-CTA globaltimer stamps (start, MMA done, epilogue done, exit) of the
+ * lane's most recent GEMM launch, [148][4] ns. */
+asb_status asb_debug_gemm_timeline(asb_lane* lane, unsigned long long* out, int n);
 asb_status asb_debug_gemm(const void* x, const void* w, const void* bias, const void* resid,
                           void* out, int tokens, int n_out, int k, int epi, int force_path,
                           int splits, void* stream);

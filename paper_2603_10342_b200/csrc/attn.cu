@@ -17,6 +17,7 @@
 #include <cfloat>
 
 #include "attn.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace asb {
@@ -115,6 +116,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();  // q / K / V were written by the kernels before us
     const int32_t* table = tables + it.table_off;
 
     if (warp == 0) {
@@ -143,6 +146,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 }
             }
         }
+        __syncwarp();  // reconverge before the CTA barrier
     } else if (warp == 1) {
         constexpr uint32_t idesc_s = make_idesc_bf16(128, kBlockTokens, false, false);
         constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
@@ -320,6 +324,8 @@ __global__ void prefill_combine_kernel(const PrefillItem* __restrict__ items,
                                        const float* __restrict__ part_o,
                                        const float* __restrict__ part_ml, int splits,
                                        __nv_bfloat16* __restrict__ out, int hq, int hkv) {
+    pdl_trigger();
+    pdl_wait();
     const PrefillItem it = items[blockIdx.x];
     const int G = hq / hkv;
     const int r = blockIdx.z, kvh = blockIdx.y, d = threadIdx.x;
@@ -356,12 +362,13 @@ cudaError_t prefill_launch(const CUtensorMap& tq, const CUtensorMap& tk, const C
     const int bps = (max_blocks + splits - 1) / splits;
     splits = (max_blocks + bps - 1) / bps;
     dim3 grid(n_items, s.hkv, splits);
-    prefill_attention_kernel<HD><<<grid, kPThreads, C::kSmem, stream>>>(tq, tk, tv, items, tables,
-                                                                       out, part_o, part_ml, bps, s);
-    if (splits > 1)
-        prefill_combine_kernel<HD><<<dim3(n_items, s.hkv, 128), HD, 0, stream>>>(
-            items, part_o, part_ml, splits, out, s.hq, s.hkv);
-    return cudaGetLastError();
+    cudaError_t e = launch_k(prefill_attention_kernel<HD>, grid, dim3(kPThreads), C::kSmem, stream, tq, tk, tv,
+                             items, tables, out, part_o, part_ml, bps, s);
+    if (e == cudaSuccess && splits > 1)
+        e = launch_k(prefill_combine_kernel<HD>, dim3(n_items, s.hkv, 128), dim3(HD), 0, stream, items,
+                     static_cast<const float*>(part_o), static_cast<const float*>(part_ml), splits, out, s.hq,
+                     s.hkv);
+    return e;
 }
 
 }  // namespace

@@ -26,6 +26,7 @@
 #include <cstdlib>
 
 #include "attn.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace asb {
@@ -129,6 +130,8 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         fence_barrier_init();
     }
     __syncthreads();
+    pdl_trigger();
+    pdl_wait();  // q and the appended K/V come from the kernel before us
 
     if (warp == kWarpsR) {
         // ------------------------------------------------------------ producer
@@ -298,6 +301,8 @@ __global__ void decode_combine_kernel(const DecodeItem* __restrict__ items,
                                       const float* __restrict__ part_o,
                                       const float* __restrict__ part_ml, int splits,
                                       __nv_bfloat16* __restrict__ out, int hq) {
+    pdl_trigger();
+    pdl_wait();
     const int row = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
     const size_t base = ((size_t)row * hq + h) * splits;
     float M = -FLT_MAX;
@@ -330,11 +335,12 @@ cudaError_t launch_hd(const CUtensorMap& tk, const CUtensorMap& tv, const __nv_b
         attr = true;
     }
     dim3 grid(n_items, s.hkv, splits);
-    decode_attn_kernel<HD><<<grid, (warps + 1) * 32, smem, st>>>(tk, tv, q, items, tables, out, po, pml, sps,
-                                                               stages, s);
-    if (splits > 1)
-        decode_combine_kernel<HD><<<dim3(n_items, s.hq), HD, 0, st>>>(items, po, pml, splits, out, s.hq);
-    return cudaGetLastError();
+    cudaError_t e = launch_k(decode_attn_kernel<HD>, grid, dim3((warps + 1) * 32), smem, st, tk, tv, q, items,
+                             tables, out, po, pml, sps, stages, s);
+    if (e == cudaSuccess && splits > 1)
+        e = launch_k(decode_combine_kernel<HD>, dim3(n_items, s.hq), dim3(HD), 0, st, items,
+                     static_cast<const float*>(po), static_cast<const float*>(pml), splits, out, s.hq);
+    return e;
 }
 
 }  // namespace

@@ -10,6 +10,7 @@
 
 #include "attn.h"
 #include "ew.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace asb {
@@ -23,9 +24,16 @@ __device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
 }
 
 // element i of a named tensor: the (i+1)-th draw of Rng::substream(seed, name)
-// (/root/reference/proj/src/rng.hpp:28-37), mapped to a uniform bf16.
+// (/root/reference/proj/src/rng.hpp:28-37), mapped to a uniform bf16.  Source row r lands on
+// logical row R = r*row_mult + row_off of the destination; with kb > 0 the destination is a
+// tile-packed weight ([N/128][K/64][128][64], see runtime.h) of K = 64*kb columns.
+__device__ __forceinline__ size_t packed_off(int64_t R, int64_t c, int kb, int dst_cols) {
+    if (kb <= 0) return static_cast<size_t>(R) * dst_cols + c;
+    return ((static_cast<size_t>(R >> 7) * kb + (c >> 6)) * 128 + (R & 127)) * 64 + (c & 63);
+}
+
 __global__ void init_weights_kernel(__nv_bfloat16* dst, uint64_t state0, int64_t rows, int cols,
-                                    int row_mult, int row_off, int dst_cols, float offset,
+                                    int row_mult, int row_off, int dst_cols, int kb, float offset,
                                     float amp_scaled) {
     const int64_t n = rows * cols;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -34,28 +42,49 @@ __global__ void init_weights_kernel(__nv_bfloat16* dst, uint64_t state0, int64_t
         const int32_t t = static_cast<int32_t>(u >> 40) - 8388608;
         const float v = __fadd_rn(offset, __fmul_rn(static_cast<float>(t), amp_scaled));
         const int64_t r = i / cols, c = i % cols;
-        dst[(r * row_mult + row_off) * dst_cols + c] = __float2bfloat16_rn(v);
+        dst[packed_off(r * row_mult + row_off, c, kb, dst_cols)] = __float2bfloat16_rn(v);
     }
 }
 
+// row-major [rows][cols] -> tile-packed (used for externally supplied weights)
+__global__ void pack_weights_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                    int64_t rows, int cols) {
+    const int64_t n = rows * cols;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / cols, c = i % cols;
+        dst[packed_off(r, c, cols / 64, cols)] = src[i];
+    }
+}
+
+// Embedding gather from the tile-packed table: a row is d/64 contiguous 128-byte chunks.
 __global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ emb,
                              __nv_bfloat16* __restrict__ x, int T, int d) {
+    pdl_trigger();
+    pdl_wait();
     const int t = blockIdx.x;
     if (t >= T) return;
-    const uint4* src = reinterpret_cast<const uint4*>(emb + static_cast<size_t>(ids[t]) * d);
+    const int64_t R = ids[t];
+    const int kb = d / 64;
     uint4* dst = reinterpret_cast<uint4*>(x + static_cast<size_t>(t) * d);
-    for (int i = threadIdx.x; i < d / 8; i += blockDim.x) dst[i] = src[i];
+    for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
+        const int chunk = i >> 3, piece = i & 7;
+        dst[i] = *reinterpret_cast<const uint4*>(emb + packed_off(R, chunk * 64 + piece * 8, kb, d));
+    }
 }
 
 // One warp per row; y = bf16(x * (1/sqrt(mean(x^2)+eps)) * w).  rows_idx (optional)
 // gathers input rows (final norm of the logit rows only).
 __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ rows_idx,
                                const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y,
-                               int n_rows, int d, float eps) {
+                               int n_rows, int d, float eps, unsigned long long* __restrict__ zero_keys) {
+    pdl_trigger();
+    pdl_wait();
     const int warps = blockDim.x >> 5;
     const int row = blockIdx.x * warps + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= n_rows) return;
+    if (zero_keys && lane == 0) zero_keys[row] = 0ull;  // argmax accumulator of the next GEMM
     const int src_row = rows_idx ? rows_idx[row] : row;
     const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(src_row) * d);
     const uint4* wr = reinterpret_cast<const uint4*>(w);
@@ -99,6 +128,8 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv,
                                    __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_pool,
                                    __nv_bfloat16* __restrict__ v_pool, int T, int hq, int hkv, int hd,
                                    int layer, int num_blocks) {
+    pdl_trigger();
+    pdl_wait();
     const int t = blockIdx.x;
     if (t >= T) return;
     const int half = hd / 2;
@@ -136,83 +167,63 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv,
     }
 }
 
-// Greedy argmax per logits row (lowest index wins ties).  One CTA per row.
+// Greedy argmax per logits row (lowest index wins ties) as an argmax_key.  One CTA per row.
+// Only for logit batches the fused LM-head epilogue does not cover (> 256 rows).
 __global__ void argmax_kernel(const float* __restrict__ logits, int V, int ld,
-                              int32_t* __restrict__ out_ids, float* __restrict__ out_max) {
-    const int row = blockIdx.x;
-    const float* lr = logits + static_cast<size_t>(row) * ld;
-    float best = -FLT_MAX;
-    int best_i = 0x7fffffff;
-    for (int i = threadIdx.x; i < V; i += blockDim.x) {
-        const float v = lr[i];
-        if (v > best) {  // strided scan in increasing i: first max is the lowest index
-            best = v;
-            best_i = i;
-        }
-    }
+                              unsigned long long* __restrict__ out_keys) {
+    pdl_trigger();
+    pdl_wait();
+    const float* lr = logits + static_cast<size_t>(blockIdx.x) * ld;
+    unsigned long long best = 0ull;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) best = max(best, argmax_key(lr[i], i));
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-        if (ob > best || (ob == best && oi < best_i)) {
-            best = ob;
-            best_i = oi;
-        }
-    }
-    __shared__ float sb[32];
-    __shared__ int si[32];
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    __shared__ unsigned long long sb[32];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) {
-        sb[w] = best;
-        si[w] = best_i;
-    }
+    if (l == 0) sb[w] = best;
     __syncthreads();
     if (w == 0) {
-        const int nw = blockDim.x >> 5;
-        best = l < nw ? sb[l] : -FLT_MAX;
-        best_i = l < nw ? si[l] : 0x7fffffff;
+        best = l < static_cast<int>(blockDim.x >> 5) ? sb[l] : 0ull;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-            if (ob > best || (ob == best && oi < best_i)) {
-                best = ob;
-                best_i = oi;
-            }
-        }
-        if (l == 0) {
-            out_ids[row] = best_i;
-            if (out_max) out_max[row] = best;
-        }
+        for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (l == 0) out_keys[blockIdx.x] = best;
     }
 }
 
 }  // namespace
 
 cudaError_t init_weights(__nv_bfloat16* dst, uint64_t state0, int64_t rows, int cols, int row_mult,
-                         int row_off, float offset, float amp, cudaStream_t stream) {
+                         int row_off, int packed_kb, float offset, float amp, cudaStream_t stream) {
     const int64_t n = rows * cols;
     int blocks = static_cast<int>((n + 255) / 256);
     if (blocks > 148 * 32) blocks = 148 * 32;
     init_weights_kernel<<<blocks, 256, 0, stream>>>(dst, state0, rows, cols, row_mult, row_off, cols,
-                                                    offset, amp * (1.0f / 8388608.0f));
+                                                    packed_kb, offset, amp * (1.0f / 8388608.0f));
+    return cudaGetLastError();
+}
+
+cudaError_t pack_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, int64_t rows, int cols,
+                         cudaStream_t stream) {
+    const int64_t n = rows * cols;
+    int blocks = static_cast<int>((n + 255) / 256);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    pack_weights_kernel<<<blocks, 256, 0, stream>>>(src, dst, rows, cols);
     return cudaGetLastError();
 }
 
 cudaError_t embed(const int32_t* ids, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int d,
                   cudaStream_t stream) {
     if (T <= 0) return cudaSuccess;
-    embed_kernel<<<T, 128, 0, stream>>>(ids, emb, x, T, d);
-    return cudaGetLastError();
+    return launch_k(embed_kernel, dim3(T), dim3(128), 0, stream, ids, emb, x, T, d);
 }
 
 cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows_idx, const __nv_bfloat16* w,
-                    __nv_bfloat16* y, int n_rows, int d, float eps, cudaStream_t stream) {
+                    __nv_bfloat16* y, int n_rows, int d, float eps, cudaStream_t stream,
+                    unsigned long long* zero_keys) {
     if (n_rows <= 0) return cudaSuccess;
     const int warps = 8;
-    rmsnorm_kernel<<<(n_rows + warps - 1) / warps, warps * 32, 0, stream>>>(x, rows_idx, w, y, n_rows,
-                                                                          d, eps);
-    return cudaGetLastError();
+    return launch_k(rmsnorm_kernel, dim3((n_rows + warps - 1) / warps), dim3(warps * 32), 0, stream, x,
+                    rows_idx, w, y, n_rows, d, eps, zero_keys);
 }
 
 cudaError_t rope_append(const __nv_bfloat16* qkv, const int32_t* pos, const int32_t* slot,
@@ -220,16 +231,14 @@ cudaError_t rope_append(const __nv_bfloat16* qkv, const int32_t* pos, const int3
                         __nv_bfloat16* k_pool, __nv_bfloat16* v_pool, int T, int hq, int hkv, int hd,
                         int layer, int num_blocks, cudaStream_t stream) {
     if (T <= 0) return cudaSuccess;
-    rope_append_kernel<<<T, 256, 0, stream>>>(qkv, pos, slot, cos_t, sin_t, q_out, k_pool, v_pool, T,
-                                             hq, hkv, hd, layer, num_blocks);
-    return cudaGetLastError();
+    return launch_k(rope_append_kernel, dim3(T), dim3(256), 0, stream, qkv, pos, slot, cos_t, sin_t, q_out,
+                    k_pool, v_pool, T, hq, hkv, hd, layer, num_blocks);
 }
 
-cudaError_t argmax_rows(const float* logits, int rows, int V, int ld, int32_t* out_ids,
-                        float* out_max, cudaStream_t stream) {
+cudaError_t argmax_rows(const float* logits, int rows, int V, int ld, unsigned long long* out_keys,
+                        cudaStream_t stream) {
     if (rows <= 0) return cudaSuccess;
-    argmax_kernel<<<rows, 1024, 0, stream>>>(logits, V, ld, out_ids, out_max);
-    return cudaGetLastError();
+    return launch_k(argmax_kernel, dim3(rows), dim3(1024), 0, stream, logits, V, ld, out_keys);
 }
 
 }  // namespace asb

@@ -5,22 +5,32 @@
 // (decode_step_duration_ms, /root/reference/proj/src/executor.cpp:207-220, and the
 // prefill rate x length arithmetic, /root/reference/proj/src/engine.cpp:450-475).
 //
-// Structure (one CTA per SM, persistent over work units):
+// Structure (192 threads, one CTA per SM):
 //   warp 0      : TMA producer   (A/B tiles -> smem ring, SWIZZLE_128B, mbarrier tx)
 //   warp 1      : MMA issuer     (one elected lane, tcgen05.mma kind::f16, commit)
 //   warps 2..5  : epilogue       (tcgen05.ld TMEM -> regs -> fused epilogue -> HBM)
-// TMEM holds two BN-column fp32 accumulators so the epilogue of unit i overlaps the
-// MMAs of unit i+1.
 //
 // Two operand orders:
-//   normal (prefill, many tokens):  A = X (tokens, M = 128 rows/tile), B = W (BN = 256)
+//   normal (prefill, many tokens):  A = X (tokens, M = 128 rows/tile), B = W (BN = 256/128)
 //   swap   (decode, <= 256 tokens): A = W (128 weight rows/tile),       B = X (BN = tokens)
-//     plus split-K across CTAs (fp32 atomics into a workspace, finalised by
-//     gemm_finalize_kernel) so a 9-tile projection still streams weights on all SMs.
+// and two schedules:
+//   persistent (splits == 1): CTAs stride over tiles; TMEM holds two accumulators so the
+//     epilogue of tile i overlaps the MMAs of tile i+1.
+//   cluster split-K (swap, splits = S > 1): the S CTAs of one thread-block cluster each
+//     stream 1/S of a weight tile's K range, park their fp32 partial in shared memory and
+//     reduce it through DSMEM in rank order -- a fixed summation order (bit-reproducible),
+//     no workspace, no atomics, no second launch.  This is what lets a 9-tile projection
+//     stream its weights on ~all SMs at decode batch sizes.
+// Launches carry the programmatic-dependent-launch attribute: the producer streams the first
+// ring of WEIGHT tiles before griddepcontrol.wait (weights never depend on the previous
+// kernel), so the weight fetch overlaps the tail of the kernel before it.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "gemm.h"
 #include "sm100.cuh"
@@ -41,11 +51,13 @@ struct GemmCfg {
     static constexpr int kStageBytes = kBytesA + kBytesB;
     static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : 2 * BN;  // power of two >= 32
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    // cluster split-K parks a [BN tokens][128 rows] fp32 partial in the (drained) ring
+    static_assert(BN * BM * 4 <= kStages * kStageBytes, "partial does not fit the ring");
 };
 
 __device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
-// Apply the epilogue to one output value pair-free path (all modes except SiLU).
+// Apply the epilogue to one output value (all modes except SiLU).
 struct Epi {
     GemmParams p;
 
@@ -65,51 +77,74 @@ struct Epi {
         case EPI_F32:
             p.out_f32[static_cast<size_t>(tok) * p.ldo + n] = v;
             break;
-        case EPI_ATOMIC:
-            atomicAdd(p.ws + static_cast<size_t>(tok) * p.n_out + n, v);
-            break;
         default:
             break;
         }
     }
+
+    // Swap-path pair (weight rows m, m+1; m even) for one token: SiLU consumes the pair
+    // (interleaved gate/up rows), every other mode stores two neighbouring outputs.
+    __device__ __forceinline__ void store_pair(int tok, int m, float v0, float v1) const {
+        if (tok >= p.tokens || m >= p.n_out) return;
+        const size_t o = static_cast<size_t>(tok) * p.ldo;
+        if (p.epi == EPI_SILU) {
+            p.out[o + (m >> 1)] = __float2bfloat16_rn(silu(v0) * v1);
+            return;
+        }
+        const bool two = m + 1 < p.n_out;
+        if (p.epi == EPI_BF16 && p.bias) {
+            v0 += __bfloat162float(p.bias[m]);
+            if (two) v1 += __bfloat162float(p.bias[m + 1]);
+        }
+        if (p.epi == EPI_RESID) {
+            const __nv_bfloat16* r = p.resid + static_cast<size_t>(tok) * p.ldr + m;
+            if (two && ((p.ldr & 1) == 0)) {
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(r);
+                v0 += bf16_lo(w);
+                v1 += bf16_hi(w);
+            } else {
+                v0 += __bfloat162float(r[0]);
+                if (two) v1 += __bfloat162float(r[1]);
+            }
+        }
+        if (p.epi == EPI_F32) {
+            if (two && ((p.ldo & 1) == 0)) {
+                *reinterpret_cast<float2*>(p.out_f32 + o + m) = make_float2(v0, v1);
+            } else {
+                p.out_f32[o + m] = v0;
+                if (two) p.out_f32[o + m + 1] = v1;
+            }
+            return;
+        }
+        if (two && ((p.ldo & 1) == 0)) {
+            *reinterpret_cast<uint32_t*>(p.out + o + m) = pack_bf16(v0, v1);
+        } else {
+            p.out[o + m] = __float2bfloat16_rn(v0);
+            if (two) p.out[o + m + 1] = __float2bfloat16_rn(v1);
+        }
+    }
 };
 
-// Work decomposition shared by the producer, MMA and epilogue roles.
-//  classic : units (tile, split) strided over the persistent grid
-//  stream-K: CTA b owns the contiguous range [b*W/grid, (b+1)*W/grid) of the flattened
-//            (tile, k-block) space (W = tiles * k_blocks), so every CTA streams the same
-//            number of k-blocks; tile boundaries inside a range flush through fp32 atomics.
+// Work decomposition shared by the producer, MMA and epilogue roles: units (tile, split)
+// strided over the grid.  splits == 1: persistent over tiles.  splits > 1: grid == units,
+// one unit per CTA, and the S splits of a tile are the S CTAs of one cluster (rank = split).
 struct Work {
-    int tiles_m, k_blocks, units, splits, kbps, streamk, u;
-    long long pos, hi;
+    int tiles_m, k_blocks, units, splits, kbps, u;
     __device__ void init(const GemmParams& p, int tm_, int tn_, int kb) {
         tiles_m = tm_;
         k_blocks = kb;
-        splits = p.splits;
-        kbps = p.kb_per_split;
-        streamk = p.streamk;
-        units = tm_ * tn_ * p.splits;
+        splits = p.splits > 1 ? p.splits : 1;
+        kbps = splits > 1 ? p.kb_per_split : kb;
+        units = tm_ * tn_ * splits;
         u = blockIdx.x;
-        const long long total = static_cast<long long>(tm_) * tn_ * kb;
-        pos = total * blockIdx.x / gridDim.x;
-        hi = total * (blockIdx.x + 1) / gridDim.x;
     }
     __device__ bool next(int& tm, int& tn, int& kb0, int& kb1) {
-        int tile;
-        if (streamk) {
-            if (pos >= hi) return false;
-            tile = static_cast<int>(pos / k_blocks);
-            kb0 = static_cast<int>(pos % k_blocks);
-            kb1 = static_cast<int>(min(static_cast<long long>(k_blocks), kb0 + (hi - pos)));
-            pos += kb1 - kb0;
-        } else {
-            if (u >= units) return false;
-            const int split = u % splits;
-            tile = u / splits;
-            kb0 = split * kbps;
-            kb1 = min(k_blocks, kb0 + kbps);
-            u += gridDim.x;
-        }
+        if (u >= units) return false;
+        const int split = u % splits;
+        const int tile = u / splits;
+        kb0 = split * kbps;
+        kb1 = min(k_blocks, kb0 + kbps);
+        u += gridDim.x;
         tm = tile % tiles_m;
         tn = tile / tiles_m;
         return true;
@@ -131,9 +166,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull_bar = empty_bar + C::kStages;
     uint64_t* tempty_bar = tfull_bar + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    float* part = reinterpret_cast<float*>(smem);  // cluster split-K partial [BN][128]
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
+    const bool clustered = p.swap && p.splits > 1;
+    auto stamp = [&](int k) {
+        if (p.dbg_times) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            p.dbg_times[blockIdx.x * 8 + k] = t;
+        }
+    };
+    if (threadIdx.x == 0) stamp(0);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmap_a);
@@ -155,6 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) stamp(6);
+    pdl_trigger();
 
     const int tiles_m = (p.M + BM - 1) / BM;
     const int tiles_n = (p.N + BN - 1) / BN;
@@ -166,20 +213,56 @@ __global__ void __launch_bounds__(kThreads, 1)
             // tiny activation operand is shared by all -> evict-last.  normal (prefill): a
             // weight tile is re-read by every M-tile in flight and the activation panel by
             // every N-tile, so both are kept (evict-last).
-            const uint64_t pol_stream = p.swap ? policy_evict_first() : policy_evict_last();
-            const uint64_t pol_keep = policy_evict_last();
-            uint32_t stage = 0, phase = 0;
+            const uint64_t pol_w = p.swap ? policy_evict_first() : policy_evict_last();
+            const uint64_t pol_x = policy_evict_last();
+            // Weight operand: A in swap, B in normal.  Activations: the other one.
+            auto load_w = [&](int stage, int kb, int tm, int tn) {
+                if (p.swap) {
+                    if (p.a_packed)
+                        tma_load_4d_hint(smem_a + stage * C::kBytesA, &tmap_a, &full_bar[stage], 0, 0, kb, tm, pol_w);
+                    else
+                        tma_load_2d_hint(smem_a + stage * C::kBytesA, &tmap_a, &full_bar[stage], kb * BK, tm * BM, pol_w);
+                } else {
+                    if (p.b_packed)
+                        tma_load_4d_hint(smem_b + stage * C::kBytesB, &tmap_b, &full_bar[stage], 0, 0, kb,
+                                         tn * (BN / 128), pol_w);
+                    else
+                        tma_load_2d_hint(smem_b + stage * C::kBytesB, &tmap_b, &full_bar[stage], kb * BK, tn * BN, pol_w);
+                }
+            };
+            auto load_x = [&](int stage, int kb, int tm, int tn) {
+                if (p.swap)
+                    tma_load_2d_hint(smem_b + stage * C::kBytesB, &tmap_b, &full_bar[stage], kb * BK, tn * BN, pol_x);
+                else
+                    tma_load_2d_hint(smem_a + stage * C::kBytesA, &tmap_a, &full_bar[stage], kb * BK, tm * BM, pol_x);
+            };
             Work w;
             w.init(p, tiles_m, tiles_n, k_blocks);
+            // Weights do not depend on the previous kernel: fill the first ring with weight
+            // tiles, then wait for the producer of our activations.
+            int pre = 0;
+            {
+                Work w0 = w;
+                int tm, tn, kb0, kb1;
+                if (w0.next(tm, tn, kb0, kb1)) {
+                    for (int kb = kb0; kb < kb1 && pre < C::kStages; ++kb, ++pre) {
+                        mbar_expect_tx(&full_bar[pre], C::kStageBytes);
+                        load_w(pre, kb, tm, tn);
+                    }
+                }
+            }
+            pdl_wait();
+            uint32_t stage = 0, phase = 0;
+            int i = 0;
             int tm, tn, kb0, kb1;
             while (w.next(tm, tn, kb0, kb1)) {
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    mbar_wait(&empty_bar[stage], phase ^ 1);
-                    mbar_expect_tx(&full_bar[stage], C::kStageBytes);
-                    tma_load_2d_hint(smem_a + stage * C::kBytesA, &tmap_a, &full_bar[stage],
-                                     kb * BK, tm * BM, p.swap ? pol_stream : pol_keep);
-                    tma_load_2d_hint(smem_b + stage * C::kBytesB, &tmap_b, &full_bar[stage],
-                                     kb * BK, tn * BN, p.swap ? pol_keep : pol_stream);
+                for (int kb = kb0; kb < kb1; ++kb, ++i) {
+                    if (i >= pre) {
+                        mbar_wait(&empty_bar[stage], phase ^ 1);
+                        mbar_expect_tx(&full_bar[stage], C::kStageBytes);
+                        load_w(stage, kb, tm, tn);
+                    }
+                    load_x(stage, kb, tm, tn);
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -187,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
+        __syncwarp();  // reconverge before the CTA barrier (bar.sync is warp-aligned)
     } else if (warp == 1) {
         constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
         uint32_t stage = 0, phase = 0;
@@ -202,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t d_tmem = tmem_base + ab * BN;
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(&full_bar[stage], phase);
+                if (local == 0 && kb == kb0 && lane == 0) stamp(4);
                 tc_fence_after();
                 if (elect_one()) {
                     const uint32_t a_addr = smem_u32(smem_a + stage * C::kBytesA);
@@ -223,8 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (elect_one()) umma_commit(&tfull_bar[ab]);
             __syncwarp();
         }
+        if (lane == 0) stamp(1);
     } else {
         // Epilogue warps 2..5: TMEM lane quarter = warp % 4.
+        pdl_wait();  // residual / output buffers belong to the previous kernels
         const uint32_t quarter = warp & 3;
         const uint32_t row_in_tile = quarter * 32 + lane;
         Epi epi{p};
@@ -236,11 +323,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t ab = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tfull_bar[ab], acc_phase);
+            if (local == 0 && threadIdx.x == 64) stamp(5);
             tc_fence_after();
             const int m = tm * BM + row_in_tile;
             const uint32_t t_row = tmem_base + ((quarter * 32u) << 16) + ab * BN;
+            if (clustered) {
+                // park the partial: part[tok][row], lanes = consecutive rows (conflict-free);
+                // every MMA of this CTA has completed, so the operand ring is free
+                for (int c = 0; c < BN && c < p.tokens; c += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(t_row + c, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) part[(c + j) * BM + row_in_tile] = __uint_as_float(r[j]);
+                }
+                continue;
+            }
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
+            for (int c = 0; c < BN && (!p.swap || c < p.tokens); c += 32) {
                 uint32_t r[32];
                 tmem_ld32(t_row + c, r);
                 tmem_ld_wait();
@@ -339,87 +439,149 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // swap: D[m = weight row][n = token] -> Y[token][weight row]
 #pragma unroll
                     for (int j = 0; j < 32; ++j) epi.store(n0 + j, m, __uint_as_float(r[j]));
+                    if (p.amax) {
+                        // fused greedy sample: key[j] per lane, then a butterfly reduce-scatter
+                        // leaves lane l with the max over the warp's 32 rows for token n0 + l
+                        unsigned long long k[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            k[j] = m < p.n_out ? argmax_key(__uint_as_float(r[j]), m) : 0ull;
+#pragma unroll
+                        for (int o = 16; o >= 1; o >>= 1) {
+                            const bool upper = (lane & o) != 0;
+#pragma unroll
+                            for (int i = 0; i < o; ++i) {
+                                const unsigned long long send = upper ? k[i] : k[i + o];
+                                const unsigned long long keep = upper ? k[i + o] : k[i];
+                                const unsigned long long got = __shfl_xor_sync(0xffffffffu, send, o);
+                                k[i] = keep > got ? keep : got;
+                            }
+                        }
+                        if (n0 + static_cast<int>(lane) < p.tokens && k[0]) atomicMax(p.amax + n0 + lane, k[0]);
+                    }
                 }
             }
+
             tc_fence_before();
             mbar_arrive(&tempty_bar[ab]);
         }
     }
 
+    if (threadIdx.x == 64) stamp(2);
     tc_fence_before();
-    __syncthreads();
+    if (clustered) {
+        // Reduce the tile over the cluster: CTA `rank` finishes row pairs
+        // [64*rank/S, 64*(rank+1)/S), summing the S partials in rank order.
+        cluster_sync();
+        const int S = p.splits;
+        const int rank = blockIdx.x % S;
+        const int tile = blockIdx.x / S;
+        const int p0 = (64 * rank) / S, p1 = (64 * (rank + 1)) / S, np = p1 - p0;
+        const uint32_t base = smem_u32(part);
+        Epi epi{p};
+        for (int e = threadIdx.x; e < np * p.tokens; e += kThreads) {
+            const int tok = e / np;
+            const int row = 2 * (p0 + e % np);
+            const uint32_t off = base + static_cast<uint32_t>((tok * BM + row) * 4);
+            float2 acc = make_float2(0.f, 0.f);
+            for (int q = 0; q < S; ++q) {
+                const float2 v = ld_dsmem_f2(mapa_shared(off, q));
+                acc.x += v.x;
+                acc.y += v.y;
+            }
+            const int m = (tile % tiles_m) * BM + row;
+            epi.store_pair(tok, m, acc.x, acc.y);
+            if (p.amax && m < p.n_out) {
+                unsigned long long k = argmax_key(acc.x, m);
+                if (m + 1 < p.n_out) k = max(k, argmax_key(acc.y, m + 1));
+                if (k) atomicMax(p.amax + tok, k);
+            }
+        }
+        cluster_sync();  // peers may still be reading our partial
+    } else {
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) stamp(3);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<C::kTmemCols>(tmem_base);
     }
 }
 
-// Split-K finalisation: ws (fp32 [tokens][n_out]) -> epilogue -> bf16/f32 out; zeroes ws.
-__global__ void gemm_finalize_kernel(const GemmParams p) {
-    const int cols = p.epi == EPI_SILU ? p.n_out / 2 : p.n_out;
-    const size_t total = static_cast<size_t>(p.tokens) * cols;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int tok = static_cast<int>(i / cols);
-        const int c = static_cast<int>(i % cols);
-        float* wrow = p.ws + static_cast<size_t>(tok) * p.n_out;
-        switch (p.epi) {
-        case EPI_SILU: {
-            const float g = wrow[2 * c], v = wrow[2 * c + 1];
-            wrow[2 * c] = 0.f;
-            wrow[2 * c + 1] = 0.f;
-            p.out[static_cast<size_t>(tok) * p.ldo + c] = __float2bfloat16_rn(silu(g) * v);
-            break;
-        }
-        case EPI_BF16: {
-            float v = wrow[c];
-            wrow[c] = 0.f;
-            if (p.bias) v += __bfloat162float(p.bias[c]);
-            p.out[static_cast<size_t>(tok) * p.ldo + c] = __float2bfloat16_rn(v);
-            break;
-        }
-        case EPI_RESID: {
-            float v = wrow[c];
-            wrow[c] = 0.f;
-            v += __bfloat162float(p.resid[static_cast<size_t>(tok) * p.ldr + c]);
-            p.out[static_cast<size_t>(tok) * p.ldo + c] = __float2bfloat16_rn(v);
-            break;
-        }
-        case EPI_F32: {
-            float v = wrow[c];
-            wrow[c] = 0.f;
-            p.out_f32[static_cast<size_t>(tok) * p.ldo + c] = v;
-            break;
-        }
-        default:
-            break;
-        }
+// Occupancy of S-CTA clusters of this kernel (cached per configuration).
+template <int BN>
+cudaError_t set_smem_attr();
+
+template <int BN>
+int max_active_clusters(int S, cudaStream_t stream) {
+    if (set_smem_attr<BN>() != cudaSuccess) return 0;
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({S, stream});
+    if (it != cache.end()) return it->second;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(S * 64, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = GemmCfg<BN>::kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_tn_kernel<BN>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
     }
+    cache[{S, stream}] = n;
+    return n;
+}
+
+template <int BN>
+cudaError_t set_smem_attr() {
+    static bool attr_set = false;  // per-process; harmless race (idempotent)
+    if (attr_set) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         GemmCfg<BN>::kSmemBytes);
+    if (e == cudaSuccess) attr_set = true;
+    return e;
 }
 
 template <int BN>
 cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
-                      int num_sms, cudaStream_t stream) {
+                      int num_sms, cudaStream_t stream, bool pdl) {
     using C = GemmCfg<BN>;
-    static bool attr_set = false;  // per-process; harmless race (idempotent)
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             C::kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    cudaError_t e = set_smem_attr<BN>();
+    if (e != cudaSuccess) return e;
     const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
-    int grid;
-    if (p.streamk) {
-        const long long work = static_cast<long long>(tiles) * ((p.K + BK - 1) / BK);
-        grid = static_cast<int>(std::min<long long>(num_sms, std::max<long long>(1, work / 4)));
-    } else {
-        const int units = tiles * p.splits;
-        grid = units < num_sms ? units : num_sms;
+    const bool clustered = p.swap && p.splits > 1;
+    const int grid = clustered ? tiles * p.splits : std::min(tiles, num_sms);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (clustered) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = p.splits;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
     }
-    gemm_tn_kernel<BN><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
-    return cudaGetLastError();
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, gemm_tn_kernel<BN>, ta, tb, p);
 }
 
 }  // namespace
@@ -431,38 +593,47 @@ int gemm_pick_bn(int n) {
     return 256;
 }
 
+int gemm_cluster_splits(int tiles, int k_blocks, int bn, int num_sms, cudaStream_t stream, int force) {
+    auto fits = [&](int S) {
+        if (S < 2) return true;
+        const int kbps = (k_blocks + S - 1) / S;
+        if ((S - 1) * kbps >= k_blocks) return false;  // an empty split
+        int act = 0;
+        switch (bn) {
+        case 32: act = max_active_clusters<32>(S, stream); break;
+        case 64: act = max_active_clusters<64>(S, stream); break;
+        case 128: act = max_active_clusters<128>(S, stream); break;
+        default: act = max_active_clusters<256>(S, stream); break;
+        }
+        return act >= tiles && tiles * S <= num_sms;
+    };
+    if (force > 0) {
+        int S = std::min(force, 8);
+        while (S > 1 && (S - 1) * ((k_blocks + S - 1) / S) >= k_blocks) --S;
+        return S;
+    }
+    if (tiles >= num_sms) return 1;
+    int S = std::min({8, num_sms / tiles, k_blocks});
+    while (S > 1 && !fits(S)) --S;
+    return std::max(S, 1);
+}
+
 cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int bn,
-                        int num_sms, cudaStream_t stream) {
+                        int num_sms, cudaStream_t stream, bool pdl) {
     const int k_blocks = (p.K + BK - 1) / BK;
-    if (p.streamk) {
-        p.splits = 1;
-        p.kb_per_split = k_blocks;
-    } else if (p.splits <= 1) {
+    if (!p.swap || p.splits <= 1) {
         p.splits = 1;
         p.kb_per_split = k_blocks;
     } else {
         p.kb_per_split = (k_blocks + p.splits - 1) / p.splits;
-        p.splits = (k_blocks + p.kb_per_split - 1) / p.kb_per_split;
     }
-    GemmParams kp = p;
-    const bool split = p.splits > 1 || p.streamk;
-    if (split) kp.epi = EPI_ATOMIC;
-    cudaError_t e;
     switch (bn) {
-    case 32: e = launch_bn<32>(ta, tb, kp, num_sms, stream); break;
-    case 64: e = launch_bn<64>(ta, tb, kp, num_sms, stream); break;
-    case 128: e = launch_bn<128>(ta, tb, kp, num_sms, stream); break;
-    case 256: e = launch_bn<256>(ta, tb, kp, num_sms, stream); break;
+    case 32: return launch_bn<32>(ta, tb, p, num_sms, stream, pdl);
+    case 64: return launch_bn<64>(ta, tb, p, num_sms, stream, pdl);
+    case 128: return launch_bn<128>(ta, tb, p, num_sms, stream, pdl);
+    case 256: return launch_bn<256>(ta, tb, p, num_sms, stream, pdl);
     default: return cudaErrorInvalidValue;
     }
-    if (e != cudaSuccess || !split) return e;
-    const int cols = p.epi == EPI_SILU ? p.n_out / 2 : p.n_out;
-    const long total = static_cast<long>(p.tokens) * cols;
-    int blocks = static_cast<int>((total + 255) / 256);
-    if (blocks > 4 * num_sms) blocks = 4 * num_sms;
-    if (blocks < 1) blocks = 1;
-    gemm_finalize_kernel<<<blocks, 256, 0, stream>>>(p);
-    return cudaGetLastError();
 }
 
 int gemm_smem_bytes(int bn) {

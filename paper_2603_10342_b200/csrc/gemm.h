@@ -10,15 +10,14 @@ enum EpiMode : int {
     EPI_RESID = 1,   // y = bf16(acc + resid)       (resid may alias out: in-place residual add)
     EPI_SILU = 2,    // y[:, j] = bf16(silu(acc[2j]) * acc[2j+1])  (interleaved gate/up rows)
     EPI_F32 = 3,     // y = acc (fp32)
-    EPI_ATOMIC = 4,  // internal: split-K partial sums into ws
 };
 
 struct GemmParams {
     int M, N, K;          // kernel view: D[M][N] = A[M][K] . B[N][K]^T
     int tokens, n_out;    // logical view: Y[tokens][n_out]
     int swap;             // 0: A = X, B = W.  1: A = W, B = X (Y = D^T)
-    int splits, kb_per_split;
-    int streamk;          // 1: balanced stream-K over (tile, k-block); epilogue via ws atomics
+    int splits;           // swap only: cluster split-K factor S (cluster = the S CTAs of a tile)
+    int kb_per_split;     // internal
     int epi;
     __nv_bfloat16* out;   // Y (bf16), row stride ldo
     float* out_f32;       // Y (fp32), row stride ldo
@@ -26,14 +25,25 @@ struct GemmParams {
     const __nv_bfloat16* bias;   // [n_out] or null
     const __nv_bfloat16* resid;  // [tokens][ldr]
     int ldr;
-    float* ws;            // split-K workspace fp32 [tokens][n_out], must be zero on entry
+    int a_packed, b_packed;  // operand is a tile-packed weight (4-D map, coords (0,0,kb,tile))
+    unsigned long long* amax;  // swap + EPI_F32 only, optional: per-token argmax_key accumulator
+                               // (atomicMax; zero on entry) -- the LM head's greedy sample
+    unsigned long long* dbg_times;  // optional per-CTA timeline [grid][8] (globaltimer ns)
 };
 
 int gemm_pick_bn(int n);
 int gemm_smem_bytes(int bn);
+// Cluster split-K factor for a swap-path GEMM of `tiles` weight tiles: the largest S <= 8
+// whose tiles*S clusters fit co-resident on num_sms SMs with no empty K split (1 = none).
+int gemm_cluster_splits(int tiles, int k_blocks, int bn, int num_sms, cudaStream_t stream,
+                        int force = 0);
+// pdl: launch with programmatic stream serialization (overlaps the previous kernel's tail).
 cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int bn,
-                        int num_sms, cudaStream_t stream);
+                        int num_sms, cudaStream_t stream, bool pdl = false);
 
+// 4-D map over a tile-packed weight [N/128][K/64][128][64]: box = box_tiles x [128][64], so
+// every TMA box is box_tiles contiguous 16 KiB chunks.
+bool make_tmap_packed(CUtensorMap* out, const void* base, int rows_padded, int cols, int box_tiles);
 // 3-D bf16 map over [d2][d1][d0] (d0 contiguous), box = [b2][b1][64], SWIZZLE_128B.
 bool make_tmap_bf16_3d(CUtensorMap* out, const void* base, int d0, int d1, int d2, int b1, int b2);
 // 2-D bf16 tensor map, row-major [rows][cols], box = [box_rows][64 cols], SWIZZLE_128B.

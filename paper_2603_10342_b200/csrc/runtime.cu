@@ -24,8 +24,10 @@
 #include "attn.h"
 #include "ew.h"
 #include "gemm.h"
+#include "launch.cuh"
 #include "json.hpp"
 #include "runtime.h"
+#include "sm100.cuh"
 
 using asb::kBlockTokens;
 using nlohmann::json;
@@ -166,9 +168,12 @@ static void* dmalloc(size_t bytes, std::vector<void*>& track) {
     return p;
 }
 
+// Weights are stored tile-packed, [N/128][K/64][128 rows][64 cols]: one 128x64 TMA box is a
+// contiguous 16 KiB chunk, so streaming a weight tile is a run of long sequential HBM reads
+// instead of 128 strided 128-byte pieces.
 static void weight_maps(Weight& w) {
-    if (!make_tmap_bf16(&w.map_b256, w.ptr, w.rows, w.cols, w.cols, 256) ||
-        !make_tmap_bf16(&w.map_a128, w.ptr, w.rows, w.cols, w.cols, 128))
+    if (!make_tmap_packed(&w.map_b256, w.ptr, w.rows_pad, w.cols, 2) ||
+        !make_tmap_packed(&w.map_a128, w.ptr, w.rows_pad, w.cols, 1))
         fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for a weight");
 }
 
@@ -201,10 +206,18 @@ struct asb_model {
 
 namespace {
 
+// vectors (norms, biases): row-major
 void fill(const asb_model* m, __nv_bfloat16* dst, const std::string& name, int64_t rows, int cols,
           int row_mult, int row_off, float offset, float amp) {
-    cuda_check(init_weights(dst, substream_state(m->seed, name), rows, cols, row_mult, row_off, offset,
+    cuda_check(init_weights(dst, substream_state(m->seed, name), rows, cols, row_mult, row_off, 0, offset,
                             amp, nullptr),
+               "init_weights");
+}
+// matrices: tile-packed; source row r -> logical row r*row_mult + row_off of w
+void fillw(const asb_model* m, const Weight& w, const std::string& name, int64_t rows, int row_mult,
+           int row_off) {
+    cuda_check(init_weights(w.ptr, substream_state(m->seed, name), rows, w.cols, row_mult, row_off,
+                            w.cols / 64, 0.f, 0.034641016f, nullptr),
                "init_weights");
 }
 
@@ -254,12 +267,14 @@ struct asb_lane {
     bool own_stream = false;
     int max_T = 0, max_segs = 0, max_tbl = 0, max_pitems = 0, max_splits = 16;
     __nv_bfloat16 *x, *h, *qkv, *q, *attn, *act, *hl;
-    float *logits, *ws, *part_o, *part_ml, *ppart_o, *ppart_ml;
+    float *logits, *part_o, *part_ml, *ppart_o, *ppart_ml;
+    bool pdl = std::getenv("ASB_NO_PDL") == nullptr;  // programmatic dependent launch
+    unsigned long long* dbg_times = nullptr;  // ASB_GEMM_TIMELINE: per-CTA stamps of the last GEMM
     size_t ppart_rows = 0;
     int32_t* d_meta = nullptr;
     int32_t* h_meta = nullptr;
-    int32_t* d_out = nullptr;
-    int32_t* h_out = nullptr;
+    unsigned long long* d_out = nullptr;  // per logit row argmax_key (fused into the LM head)
+    unsigned long long* h_out = nullptr;
     size_t meta_ints = 0;
     std::vector<void*> allocs;
     // tensor maps of GEMM inputs: [0] box 128 (normal A), [1..4] box 32/64/128/256 (swap B)
@@ -349,8 +364,10 @@ int swap_map_index(int bn) { return bn == 32 ? 1 : bn == 64 ? 2 : bn == 128 ? 3 
 // Y[T][n_out] = X[T][k] . W^T with the path chosen by T.
 void linear(asb_lane* L, const CUtensorMap* xmaps, const Weight& w, int T, int epi,
             __nv_bfloat16* out, int ldo, const __nv_bfloat16* bias, const __nv_bfloat16* resid,
-            float* out_f32, int force_path = -1, int force_splits = 0) {
+            float* out_f32, int force_path = -1, int force_splits = 0,
+            unsigned long long* amax = nullptr) {
     GemmParams p{};
+    p.amax = amax;
     p.tokens = T;
     p.n_out = w.rows;
     p.K = w.cols;
@@ -361,7 +378,7 @@ void linear(asb_lane* L, const CUtensorMap* xmaps, const Weight& w, int T, int e
     p.bias = bias;
     p.resid = resid;
     p.ldr = ldo;
-    p.ws = L->ws;
+    p.dbg_times = L->dbg_times;
     const int num_sms = L->n_sms();
     L->n_launch += 1;
     const bool swap = force_path >= 0 ? force_path == 1 : T <= 256;
@@ -370,24 +387,22 @@ void linear(asb_lane* L, const CUtensorMap* xmaps, const Weight& w, int T, int e
     const double units = swap ? 2.0 * (double(w.rows) * w.cols + double(T) * w.cols) +
                                     double(T) * w.rows * (epi == EPI_F32 ? 4.0 : 2.0)
                               : 2.0 * T * double(w.rows) * w.cols;
+    const bool pdl = tl_pdl;
     L->timed(swap ? ASB_STAT_DECODE_GEMM : ASB_STAT_PREFILL_GEMM, units, [&] {
     if (swap) {
         const int bn = gemm_pick_bn(T);
         p.swap = 1;
+        p.a_packed = 1;
         p.M = w.rows;
         p.N = T;
         const int tiles = (w.rows + 127) / 128;
         const int kb = (w.cols + 63) / 64;
-        int splits = force_splits > 0 ? force_splits : (num_sms + tiles - 1) / tiles;
-        if (force_splits <= 0) splits = std::min(splits, std::max(1, kb / 4));
-        if (epi == EPI_F32 && force_splits <= 0) splits = 1;
-        p.splits = splits;
-        // balanced stream-K whenever whole tiles would leave a ragged last wave (the fp32
-        // workspace holds <= 256 token rows; the LM head writes fp32 logits directly)
-        p.streamk = (force_splits <= 0 && epi != EPI_F32 && (tiles % num_sms) != 0 && tiles < 8 * num_sms) ? 1 : 0;
-        e = gemm_launch(w.map_a128, xmaps[swap_map_index(bn)], p, bn, num_sms, L->stream);
+        // fewer weight tiles than SMs: split K over an S-CTA cluster per tile (DSMEM reduce)
+        p.splits = gemm_cluster_splits(tiles, kb, bn, num_sms, L->stream, force_splits);
+        e = gemm_launch(w.map_a128, xmaps[swap_map_index(bn)], p, bn, num_sms, L->stream, pdl);
     } else {
         p.swap = 0;
+        p.b_packed = 1;
         p.M = T;
         p.N = w.rows;
         const int tm = (T + 127) / 128;
@@ -395,7 +410,7 @@ void linear(asb_lane* L, const CUtensorMap* xmaps, const Weight& w, int T, int e
         const int bn = (t256 < (num_sms * 4) / 5) ? 128 : 256;
         p.splits = 1;
         // normal path: B = W.  bn==128 reuses the box-128 weight map.
-        e = gemm_launch(xmaps[0], bn == 256 ? w.map_b256 : w.map_a128, p, bn, num_sms, L->stream);
+        e = gemm_launch(xmaps[0], bn == 256 ? w.map_b256 : w.map_a128, p, bn, num_sms, L->stream, pdl);
     }
     });
     cuda_check(e, "gemm launch");
@@ -451,8 +466,10 @@ asb_status asb_model_create(const char* model, uint64_t seed, int device, int ma
         auto mk = [&](int rows, int cols) {
             Weight w;
             w.rows = rows;
+            w.rows_pad = (rows + 127) / 128 * 128;
             w.cols = cols;
-            w.ptr = static_cast<__nv_bfloat16*>(dmalloc(size_t(rows) * cols * 2, m->allocs));
+            w.ptr = static_cast<__nv_bfloat16*>(dmalloc(size_t(w.rows_pad) * cols * 2, m->allocs));
+            cuda_check(cudaMemset(w.ptr, 0, size_t(w.rows_pad) * cols * 2), "memset weight");
             return w;
         };
         auto vec = [&](int n) {
@@ -460,13 +477,13 @@ asb_status asb_model_create(const char* model, uint64_t seed, int device, int ma
         };
         const int qd = s.hq * s.hd, kvd = s.hkv * s.hd;
         m->embed = mk(s.vocab, s.d);
-        fill(m.get(), m->embed.ptr, "embed", s.vocab, s.d, 1, 0, 0.f, kAmpW);
+        fillw(m.get(), m->embed, "embed", s.vocab, 1, 0);
         weight_maps(m->embed);
         if (s.tied) {
             m->lm_head = m->embed;
         } else {
             m->lm_head = mk(s.vocab, s.d);
-            fill(m.get(), m->lm_head.ptr, "lm_head", s.vocab, s.d, 1, 0, 0.f, kAmpW);
+            fillw(m.get(), m->lm_head, "lm_head", s.vocab, 1, 0);
             weight_maps(m->lm_head);
         }
         m->final_norm = vec(s.d);
@@ -479,9 +496,9 @@ asb_status asb_model_create(const char* model, uint64_t seed, int device, int ma
             ly.mlp_norm = vec(s.d);
             fill(m.get(), ly.mlp_norm, p + "mlp_norm", 1, s.d, 1, 0, 1.f, kAmpN);
             ly.qkv = mk(qd + 2 * kvd, s.d);
-            fill(m.get(), ly.qkv.ptr, p + "q", qd, s.d, 1, 0, 0.f, kAmpW);
-            fill(m.get(), ly.qkv.ptr + size_t(qd) * s.d, p + "k", kvd, s.d, 1, 0, 0.f, kAmpW);
-            fill(m.get(), ly.qkv.ptr + size_t(qd + kvd) * s.d, p + "v", kvd, s.d, 1, 0, 0.f, kAmpW);
+            fillw(m.get(), ly.qkv, p + "q", qd, 1, 0);
+            fillw(m.get(), ly.qkv, p + "k", kvd, 1, qd);
+            fillw(m.get(), ly.qkv, p + "v", kvd, 1, qd + kvd);
             weight_maps(ly.qkv);
             ly.qkv_bias = nullptr;
             if (s.qkv_bias) {
@@ -491,15 +508,15 @@ asb_status asb_model_create(const char* model, uint64_t seed, int device, int ma
                 fill(m.get(), ly.qkv_bias + qd + kvd, p + "v_bias", 1, kvd, 1, 0, 0.f, kAmpB);
             }
             ly.o = mk(s.d, qd);
-            fill(m.get(), ly.o.ptr, p + "o", s.d, qd, 1, 0, 0.f, kAmpW);
+            fillw(m.get(), ly.o, p + "o", s.d, 1, 0);
             weight_maps(ly.o);
             // gate/up interleaved: row 2j = gate_j, row 2j+1 = up_j (SiLU·mul epilogue pairs)
             ly.gate_up = mk(2 * s.ffn, s.d);
-            fill(m.get(), ly.gate_up.ptr, p + "gate", s.ffn, s.d, 2, 0, 0.f, kAmpW);
-            fill(m.get(), ly.gate_up.ptr, p + "up", s.ffn, s.d, 2, 1, 0.f, kAmpW);
+            fillw(m.get(), ly.gate_up, p + "gate", s.ffn, 2, 0);
+            fillw(m.get(), ly.gate_up, p + "up", s.ffn, 2, 1);
             weight_maps(ly.gate_up);
             ly.down = mk(s.d, s.ffn);
-            fill(m.get(), ly.down.ptr, p + "down", s.d, s.ffn, 1, 0, 0.f, kAmpW);
+            fillw(m.get(), ly.down, p + "down", s.d, 1, 0);
             weight_maps(ly.down);
             m->layers.push_back(ly);
         }
@@ -716,10 +733,8 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->act = bf(size_t(T) * s.ffn);
         L->hl = bf(size_t(L->max_segs) * s.d);
         L->logits = static_cast<float*>(dmalloc(size_t(L->max_segs) * s.vocab * 4, L->allocs));
-        const int ws_rows = std::min(T, 256);
-        const size_t ws_cols = std::max<size_t>({size_t(2) * s.ffn, size_t(qd + 2 * kvd), size_t(s.d)});
-        L->ws = static_cast<float*>(dmalloc(size_t(ws_rows) * ws_cols * 4, L->allocs));
-        cuda_check(cudaMemset(L->ws, 0, size_t(ws_rows) * ws_cols * 4), "memset ws");
+        if (std::getenv("ASB_GEMM_TIMELINE"))
+            L->dbg_times = static_cast<unsigned long long*>(dmalloc(148 * 8 * 8, L->allocs));
         const int dec_rows = std::min(L->max_segs, T);
         L->part_o = static_cast<float*>(
             dmalloc(size_t(dec_rows) * s.hq * L->max_splits * s.hd * 4, L->allocs));
@@ -733,8 +748,8 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
                        4 * size_t(L->max_pitems) + 64;
         L->d_meta = static_cast<int32_t*>(dmalloc(L->meta_ints * 4, L->allocs));
         cuda_check(cudaMallocHost(&L->h_meta, L->meta_ints * 4), "cudaMallocHost");
-        L->d_out = static_cast<int32_t*>(dmalloc(size_t(L->max_segs) * 4, L->allocs));
-        cuda_check(cudaMallocHost(&L->h_out, size_t(L->max_segs) * 4), "cudaMallocHost");
+        L->d_out = static_cast<unsigned long long*>(dmalloc(size_t(L->max_segs) * 8, L->allocs));
+        cuda_check(cudaMallocHost(&L->h_out, size_t(L->max_segs) * 8), "cudaMallocHost");
         act_maps(L->map_h, L->h, T, s.d);
         act_maps(L->map_attn, L->attn, T, qd);
         act_maps(L->map_act, L->act, T, s.ffn);
@@ -891,6 +906,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         if (L->prof && !L->marks.empty()) L->resolve_marks();
         cudaEvent_t fwd_a = L->prof ? L->take_event() : nullptr;
         if (fwd_a) cuda_check(cudaEventRecord(fwd_a, st), "event");
+        PdlScope pdl_scope(L->pdl && !L->prof);
         cuda_check(embed(d_tok, m->embed.ptr, L->x, T, s.d, st), "embed");
         for (int l = 0; l < s.layers; ++l) {
             const auto& ly = m->layers[l];
@@ -920,13 +936,18 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
             linear(L, L->map_act, ly.down, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
         }
         if (n_logit > 0) {
-            cuda_check(rmsnorm(L->x, d_lrows, m->final_norm, L->hl, n_logit, s.d, s.eps, st), "final norm");
+            // greedy sample fused into the LM head epilogue (swap path, <= 256 rows): the norm
+            // zeroes the per-row argmax keys, the GEMM atomicMax-es into them
+            const bool fused_argmax = n_logit <= 256;
+            cuda_check(rmsnorm(L->x, d_lrows, m->final_norm, L->hl, n_logit, s.d, s.eps, st,
+                               fused_argmax ? L->d_out : nullptr), "final norm");
             linear(L, L->map_hl, m->lm_head, n_logit, EPI_F32, nullptr, s.vocab, nullptr, nullptr,
-                   L->logits);
-            cuda_check(argmax_rows(L->logits, n_logit, s.vocab, s.vocab, L->d_out, nullptr, st), "argmax");
-            cuda_check(cudaMemcpyAsync(L->h_out, L->d_out, n_logit * 4, cudaMemcpyDeviceToHost, st),
+                   L->logits, -1, 0, fused_argmax ? L->d_out : nullptr);
+            if (!fused_argmax)
+                cuda_check(argmax_rows(L->logits, n_logit, s.vocab, s.vocab, L->d_out, st), "argmax");
+            cuda_check(cudaMemcpyAsync(L->h_out, L->d_out, n_logit * 8, cudaMemcpyDeviceToHost, st),
                        "ids D2H");
-            L->d2h += int64_t(n_logit) * 4;
+            L->d2h += int64_t(n_logit) * 8;
         }
         if (fwd_a) {
             cudaEvent_t fwd_b = L->take_event();
@@ -936,6 +957,21 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         cuda_check(cudaEventRecord(L->ev1, st), "event");
         L->launched = true;
         L->last_logit_rows = n_logit;
+    });
+}
+
+static unsigned long long g_timeline[148 * 8];
+
+asb_status asb_debug_gemm_timeline(asb_lane* L, unsigned long long* out, int n) {
+    if (!out) return ASB_ERR_INVALID_ARGUMENT;
+    if (!L) {  // last asb_debug_gemm call
+        std::memcpy(out, g_timeline, size_t(std::min(n, 148 * 8)) * 8);
+        return ASB_OK;
+    }
+    if (!L->dbg_times) return ASB_ERR_INVALID_ARGUMENT;
+    return guarded([&] {
+        cuda_check(cudaStreamSynchronize(L->stream), "timeline");
+        cuda_check(cudaMemcpy(out, L->dbg_times, size_t(std::min(n, 148 * 8)) * 8, cudaMemcpyDeviceToHost), "timeline");
     });
 }
 
@@ -984,7 +1020,8 @@ asb_status asb_lane_fetch(asb_lane* L, int32_t* out_next, int n, float* out_logi
         if (!L->launched) fail(ASB_ERR_NO_DATA, "nothing launched on this lane");
         cuda_check(cudaEventSynchronize(L->ev1), "lane fetch");
         if (n > L->last_logit_rows) fail(ASB_ERR_INVALID_ARGUMENT, "more ids requested than produced");
-        if (out_next) std::memcpy(out_next, L->h_out, size_t(n) * 4);
+        if (out_next)
+            for (int i = 0; i < n; ++i) out_next[i] = argmax_key_index(L->h_out[i]);
         if (out_logits)
             cuda_check(cudaMemcpy(out_logits, L->logits, size_t(n) * L->m->spec.vocab * 4,
                                   cudaMemcpyDeviceToHost),
@@ -1023,13 +1060,17 @@ asb_status asb_debug_gemm(const void* x, const void* w, const void* bias, const 
                           int splits, void* stream) {
     return guarded([&] {
         Weight W;
-        W.ptr = static_cast<__nv_bfloat16*>(const_cast<void*>(w));
         W.rows = n_out;
+        W.rows_pad = (n_out + 127) / 128 * 128;
         W.cols = k;
+        cuda_check(cudaMalloc(&W.ptr, size_t(W.rows_pad) * k * 2), "packed w");
+        cuda_check(cudaMemset(W.ptr, 0, size_t(W.rows_pad) * k * 2), "packed w");
+        cuda_check(pack_weights(static_cast<const __nv_bfloat16*>(w), W.ptr, n_out, k,
+                                static_cast<cudaStream_t>(stream)), "pack");
         weight_maps(W);
         CUtensorMap xm[5];
         act_maps(xm, x, tokens, k);
-        asb_lane tmp;  // only stream, ws and sms are used by linear()
+        asb_lane tmp;  // only stream and sms are used by linear()
         asb_model fake;
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1039,16 +1080,21 @@ asb_status asb_debug_gemm(const void* x, const void* w, const void* bias, const 
         fake.num_sms = prop.multiProcessorCount;
         tmp.m = &fake;
         tmp.stream = static_cast<cudaStream_t>(stream);
-        const int ws_rows = std::min(tokens, 256);
-        cuda_check(cudaMalloc(&tmp.ws, size_t(ws_rows) * n_out * 4), "ws");
-        cuda_check(cudaMemset(tmp.ws, 0, size_t(ws_rows) * n_out * 4), "ws");
         const int ldo = epi == EPI_SILU ? n_out / 2 : n_out;
+        if (std::getenv("ASB_GEMM_TIMELINE")) {
+            cuda_check(cudaMalloc(&tmp.dbg_times, 148 * 8 * 8), "timeline");
+            cuda_check(cudaMemset(tmp.dbg_times, 0, 148 * 8 * 8), "timeline");
+        }
         linear(&tmp, xm, W, tokens, epi, static_cast<__nv_bfloat16*>(out), ldo,
                static_cast<const __nv_bfloat16*>(bias), static_cast<const __nv_bfloat16*>(resid),
                epi == EPI_F32 ? static_cast<float*>(out) : nullptr, force_path, splits);
         cuda_check(cudaStreamSynchronize(tmp.stream), "debug gemm");
-        cudaFree(tmp.ws);
-        tmp.ws = nullptr;
+        if (tmp.dbg_times) {
+            cuda_check(cudaMemcpy(g_timeline, tmp.dbg_times, sizeof(g_timeline), cudaMemcpyDeviceToHost), "timeline");
+            cudaFree(tmp.dbg_times);
+            tmp.dbg_times = nullptr;
+        }
+        cudaFree(W.ptr);
         tmp.allocs.clear();
         fake.allocs.clear();
         tmp.m = &fake;

@@ -18,8 +18,8 @@ struct ModelSpec {
 };
 
 struct Weight {
-    __nv_bfloat16* ptr = nullptr;
-    int rows = 0, cols = 0;
+    __nv_bfloat16* ptr = nullptr;  // tile-packed [rows_pad/128][cols/64][128][64]
+    int rows = 0, rows_pad = 0, cols = 0;
     CUtensorMap map_b256;  // B operand of the normal path (box 256 rows)
     CUtensorMap map_a128;  // A operand of the swap path / B with BN=128 (box 128 rows)
 };

@@ -5,6 +5,7 @@
 // and "instruction descriptor" tables (cross-checked against CuTe's
 // UMMA::SmemDescriptor / UMMA::InstrDescriptor bitfields).
 #pragma once
+#include <cstring>
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -83,6 +84,15 @@ __device__ __forceinline__ void tma_load_2d_hint(void* dst, const void* tmap, ui
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_hint(void* dst, const void* tmap, uint64_t* bar, int x,
+                                                 int y, int z, int w, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "r"(w),
+        "l"(policy)
         : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -191,6 +201,43 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool a_mn_m
            | ((b_mn_major ? 1u : 0u) << 16)            // B major
            | (static_cast<uint32_t>(N >> 3) << 17)     // N >> 3
            | (static_cast<uint32_t>(M >> 4) << 24);    // M >> 4
+}
+
+// ---------------------------------------------------------------- clusters / DSMEM
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+// Address of the same shared-memory offset in CTA `rank` of this cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float2 ld_dsmem_f2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Block until the preceding kernel on the stream has completed and its writes are visible
+// (no-op when the launch carried no programmatic dependency).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the next kernel on the stream start launching (its prologue overlaps our tail).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---------------------------------------------------------------- greedy-argmax keys
+// Order-preserving 64-bit key: larger logit wins, ties go to the LOWER index, NaN never wins.
+// A running argmax is then one atomicMax per candidate (associative, order-independent).
+__host__ __device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
+    uint32_t f;
+    memcpy(&f, &v, 4);
+    if ((f & 0x7fffffffu) > 0x7f800000u) return 0ull;  // NaN
+    const uint32_t o = (f & 0x80000000u) ? ~f : (f | 0x80000000u);
+    return (static_cast<unsigned long long>(o) << 32) | (0xffffffffu - static_cast<uint32_t>(idx));
+}
+__host__ __device__ __forceinline__ int argmax_key_index(unsigned long long k) {
+    return static_cast<int>(0xffffffffu - static_cast<uint32_t>(k & 0xffffffffu));
 }
 
 // ---------------------------------------------------------------- misc
