@@ -32,6 +32,7 @@
 #include <mutex>
 #include <tuple>
 
+#include "attn.h"
 #include "gemm.h"
 #include "sm100.cuh"
 
@@ -125,6 +126,34 @@ struct Epi {
     }
 };
 
+// ---- fused QKV epilogue helpers (EPI_QKV) ----------------------------------------------
+__device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+__device__ __forceinline__ size_t pool_off(const RopeEpi& R, int slot, int kv_head) {
+    const int blk = slot / kBlockTokens, off = slot % kBlockTokens;
+    return ((((size_t)R.layer * R.num_blocks + blk) * R.hkv + kv_head) * kBlockTokens + off) * R.hd;
+}
+
+// rotate_half pair at one cos/sin column (same op order as rope_append_kernel)
+__device__ __forceinline__ void rope2(float x1, float x2, float c, float s, float& y1, float& y2) {
+    y1 = __fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, s));
+    y2 = __fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, s));
+}
+
+__device__ __forceinline__ void store32_bf16(__nv_bfloat16* dst, const float (&v)[32]) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        d4[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                           pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+}
+
+// Destination of the rotated head `head` (q heads first, then k heads) for one token.
+__device__ __forceinline__ __nv_bfloat16* rot_dst(const RopeEpi& R, int tok, int sl, int head) {
+    return head < R.hq ? R.q_out + ((size_t)tok * R.hq + head) * R.hd
+                       : R.k_pool + pool_off(R, sl, head - R.hq);
+}
+
 // Work decomposition shared by the producer, MMA and epilogue roles: units (tile, split)
 // strided over the grid.  splits == 1: persistent over tiles.  splits > 1: grid == units,
 // one unit per CTA, and the S splits of a tile are the S CTAs of one cluster (rank = split).
@@ -170,7 +199,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
-    const bool clustered = p.swap && p.splits > 1;
+    // staged swap epilogue: the tile's fp32 partial is parked in smem and finished from there
+    // (cluster split-K reduction over DSMEM, and/or the cross-row QKV/RoPE epilogue)
+    const bool clustered = p.swap && (p.splits > 1 || p.epi == EPI_QKV);
     auto stamp = [&](int k) {
         if (p.dbg_times) {
             unsigned long long t;
@@ -339,6 +370,63 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 continue;
             }
+            if (p.epi == EPI_QKV) {
+                // normal path (prefill): thread = token m, columns = features; one head at a
+                // time, rotate_half partners (j, j + hd/2) both come from this thread's TMEM lane
+                const RopeEpi& R = p.rope;
+                const int hd = R.hd, H = hd / 2, qd = R.hq * hd, kvd = R.hkv * hd;
+                const bool tok_ok = m < p.tokens;
+                const int sl = tok_ok ? R.slot[m] : 0;
+                const int pos = tok_ok ? R.pos[m] : 0;
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += hd) {
+                    const int f0 = tn * BN + c0;
+                    const bool ok = tok_ok && f0 < p.n_out;
+                    if (f0 >= qd + kvd) {
+#pragma unroll 1
+                        for (int c = 0; c < hd; c += 32) {
+                            uint32_t r[32];
+                            tmem_ld32(t_row + c0 + c, r);
+                            tmem_ld_wait();
+                            if (ok) {
+                                float v[32];
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    v[j] = __uint_as_float(r[j]) + (p.bias ? __bfloat162float(p.bias[f0 + c + j]) : 0.f);
+                                store32_bf16(R.v_pool + pool_off(R, sl, (f0 - qd - kvd) / hd) + c, v);
+                            }
+                        }
+                        continue;
+                    }
+                    __nv_bfloat16* dst = ok ? rot_dst(R, m, sl, f0 / hd) : nullptr;
+#pragma unroll 1
+                    for (int sub = 0; sub < H; sub += 32) {
+                        uint32_t r1[32], r2[32];
+                        tmem_ld32(t_row + c0 + sub, r1);
+                        tmem_ld32(t_row + c0 + H + sub, r2);
+                        tmem_ld_wait();
+                        if (ok) {
+                            const float* ct = R.cos_t + (size_t)pos * H + sub;
+                            const float* st = R.sin_t + (size_t)pos * H + sub;
+                            float y1[32], y2[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                float x1 = __uint_as_float(r1[j]), x2 = __uint_as_float(r2[j]);
+                                if (p.bias) {
+                                    x1 += __bfloat162float(p.bias[f0 + sub + j]);
+                                    x2 += __bfloat162float(p.bias[f0 + H + sub + j]);
+                                }
+                                rope2(bf16r(x1), bf16r(x2), ct[j], st[j], y1[j], y2[j]);
+                            }
+                            store32_bf16(dst + sub, y1);
+                            store32_bf16(dst + H + sub, y2);
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&tempty_bar[ab]);
+                continue;
+            }
 #pragma unroll 1
             for (int c = 0; c < BN && (!p.swap || c < p.tokens); c += 32) {
                 uint32_t r[32];
@@ -473,15 +561,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Reduce the tile over the cluster: CTA `rank` finishes row pairs
         // [64*rank/S, 64*(rank+1)/S), summing the S partials in rank order.
         cluster_sync();
-        const int S = p.splits;
+        const int S = p.splits > 1 ? p.splits : 1;
         const int rank = blockIdx.x % S;
         const int tile = blockIdx.x / S;
-        const int p0 = (64 * rank) / S, p1 = (64 * (rank + 1)) / S, np = p1 - p0;
         const uint32_t base = smem_u32(part);
-        Epi epi{p};
-        for (int e = threadIdx.x; e < np * p.tokens; e += kThreads) {
-            const int tok = e / np;
-            const int row = 2 * (p0 + e % np);
+        auto sum2 = [&](int tok, int row) {
             const uint32_t off = base + static_cast<uint32_t>((tok * BM + row) * 4);
             float2 acc = make_float2(0.f, 0.f);
             for (int q = 0; q < S; ++q) {
@@ -489,6 +573,66 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc.x += v.x;
                 acc.y += v.y;
             }
+            return acc;
+        };
+        if (p.epi == EPI_QKV) {
+            const RopeEpi& R = p.rope;
+            const int hd = R.hd, H = hd / 2, qd = R.hq * hd, kvd = R.hkv * hd;
+            const int f0 = (tile % tiles_m) * BM;
+            const bool vt = f0 >= qd + kvd;
+            const int per_tok = vt ? 64 : 32;  // V: row pairs; q/k: (j, j+1) x (lo, hi half) quads
+            const int n = p.tokens * per_tok;
+            const int lo = static_cast<int>((static_cast<long long>(n) * rank) / S);
+            const int hi = static_cast<int>((static_cast<long long>(n) * (rank + 1)) / S);
+            for (int e = lo + threadIdx.x; e < hi; e += kThreads) {
+                const int tok = e / per_tok, i = e % per_tok;
+                const int sl = R.slot[tok];
+                if (vt) {
+                    const int mrow = 2 * i, f = f0 + mrow;
+                    if (f >= p.n_out) continue;
+                    float2 a = sum2(tok, mrow);
+                    if (p.bias) {
+                        a.x += __bfloat162float(p.bias[f]);
+                        a.y += __bfloat162float(p.bias[f + 1]);
+                    }
+                    const int fv = f - qd - kvd;
+                    *reinterpret_cast<uint32_t*>(R.v_pool + pool_off(R, sl, fv / hd) + fv % hd) = pack_bf16(a.x, a.y);
+                } else {
+                    const int hl = i / (H / 2), j = 2 * (i % (H / 2));
+                    const int m1 = hl * hd + j, f1 = f0 + m1;
+                    if (f1 >= p.n_out) continue;
+                    float2 a = sum2(tok, m1), b = sum2(tok, m1 + H);
+                    if (p.bias) {
+                        a.x += __bfloat162float(p.bias[f1]);
+                        a.y += __bfloat162float(p.bias[f1 + 1]);
+                        b.x += __bfloat162float(p.bias[f1 + H]);
+                        b.y += __bfloat162float(p.bias[f1 + H + 1]);
+                    }
+                    const int pos = R.pos[tok];
+                    const float* ct = R.cos_t + (size_t)pos * H + j;
+                    const float* st = R.sin_t + (size_t)pos * H + j;
+                    float y1a, y2a, y1b, y2b;
+                    rope2(bf16r(a.x), bf16r(b.x), ct[0], st[0], y1a, y2a);
+                    rope2(bf16r(a.y), bf16r(b.y), ct[1], st[1], y1b, y2b);
+                    __nv_bfloat16* dst = rot_dst(R, tok, sl, (f0 + hl * hd) / hd);
+                    *reinterpret_cast<uint32_t*>(dst + j) = pack_bf16(y1a, y1b);
+                    *reinterpret_cast<uint32_t*>(dst + j + H) = pack_bf16(y2a, y2b);
+                }
+            }
+            cluster_sync();
+            if (threadIdx.x == 0) stamp(3);
+            if (warp == 1) {
+                tc_fence_after();
+                tmem_dealloc<C::kTmemCols>(tmem_base);
+            }
+            return;
+        }
+        const int p0 = (64 * rank) / S, p1 = (64 * (rank + 1)) / S, np = p1 - p0;
+        Epi epi{p};
+        for (int e = threadIdx.x; e < np * p.tokens; e += kThreads) {
+            const int tok = e / np;
+            const int row = 2 * (p0 + e % np);
+            const float2 acc = sum2(tok, row);
             const int m = (tile % tiles_m) * BM + row;
             epi.store_pair(tok, m, acc.x, acc.y);
             if (p.amax && m < p.n_out) {
@@ -558,8 +702,9 @@ cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const GemmPa
     cudaError_t e = set_smem_attr<BN>();
     if (e != cudaSuccess) return e;
     const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+    const bool staged = p.swap && (p.splits > 1 || p.epi == EPI_QKV);
     const bool clustered = p.swap && p.splits > 1;
-    const int grid = clustered ? tiles * p.splits : std::min(tiles, num_sms);
+    const int grid = staged ? tiles * std::max(1, p.splits) : std::min(tiles, num_sms);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);

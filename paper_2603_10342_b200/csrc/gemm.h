@@ -10,6 +10,21 @@ enum EpiMode : int {
     EPI_RESID = 1,   // y = bf16(acc + resid)       (resid may alias out: in-place residual add)
     EPI_SILU = 2,    // y[:, j] = bf16(silu(acc[2j]) * acc[2j+1])  (interleaved gate/up rows)
     EPI_F32 = 3,     // y = acc (fp32)
+    EPI_QKV = 4,     // fused QKV epilogue: bf16(acc + bias) -> RoPE(q, k) -> q_out / paged K,V
+};
+
+// EPI_QKV: rows of W are [q heads | k heads | v heads] x hd (qd, kvd multiples of 128); the
+// rotated q goes to q_out[tok][hq][hd], k and v to the paged pools at slot[tok]
+// (layout of attn.h).  Same rounding points as a bf16 QKV GEMM followed by rope_append.
+struct RopeEpi {
+    const int32_t* pos;    // [tokens] absolute position (cos/sin row)
+    const int32_t* slot;   // [tokens] block * kBlockTokens + offset
+    const float* cos_t;    // [max_pos][hd/2]
+    const float* sin_t;
+    __nv_bfloat16* q_out;
+    __nv_bfloat16* k_pool;
+    __nv_bfloat16* v_pool;
+    int hq, hkv, hd, layer, num_blocks;
 };
 
 struct GemmParams {
@@ -26,6 +41,7 @@ struct GemmParams {
     const __nv_bfloat16* resid;  // [tokens][ldr]
     int ldr;
     int a_packed, b_packed;  // operand is a tile-packed weight (4-D map, coords (0,0,kb,tile))
+    RopeEpi rope;              // EPI_QKV only
     unsigned long long* amax;  // swap + EPI_F32 only, optional: per-token argmax_key accumulator
                                // (atomicMax; zero on entry) -- the LM head's greedy sample
     unsigned long long* dbg_times;  // optional per-CTA timeline [grid][8] (globaltimer ns)

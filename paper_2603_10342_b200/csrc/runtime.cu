@@ -365,9 +365,10 @@ int swap_map_index(int bn) { return bn == 32 ? 1 : bn == 64 ? 2 : bn == 128 ? 3 
 void linear(asb_lane* L, const CUtensorMap* xmaps, const Weight& w, int T, int epi,
             __nv_bfloat16* out, int ldo, const __nv_bfloat16* bias, const __nv_bfloat16* resid,
             float* out_f32, int force_path = -1, int force_splits = 0,
-            unsigned long long* amax = nullptr) {
+            unsigned long long* amax = nullptr, const RopeEpi* rope = nullptr) {
     GemmParams p{};
     p.amax = amax;
+    if (rope) p.rope = *rope;
     p.tokens = T;
     p.n_out = w.rows;
     p.K = w.cols;
@@ -908,15 +909,32 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         if (fwd_a) cuda_check(cudaEventRecord(fwd_a, st), "event");
         PdlScope pdl_scope(L->pdl && !L->prof);
         cuda_check(embed(d_tok, m->embed.ptr, L->x, T, s.d, st), "embed");
+        // the fused QKV epilogue needs q/k/v regions aligned to the 128-row weight tiles
+        // ASB_DEBUG_SKIP=attn,norm,...: timing ablation only (outputs are garbage)
+        static const std::string skip_list = std::getenv("ASB_DEBUG_SKIP") ? std::getenv("ASB_DEBUG_SKIP") : "";
+        auto skip = [&](const char* what) {
+            return !skip_list.empty() && ("," + skip_list + ",").find("," + std::string(what) + ",") != std::string::npos;
+        };
+        const bool fuse_qkv = (qd % 128 == 0) && (kvd % 128 == 0) && (s.hd == 64 || s.hd == 128) &&
+                              std::getenv("ASB_NO_QKV_FUSION") == nullptr;
         for (int l = 0; l < s.layers; ++l) {
             const auto& ly = m->layers[l];
             as.layer = l;
-            cuda_check(rmsnorm(L->x, nullptr, ly.attn_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
-            linear(L, L->map_h, ly.qkv, T, EPI_BF16, L->qkv, qd + 2 * kvd, ly.qkv_bias, nullptr, nullptr);
-            cuda_check(rope_append(L->qkv, d_pos, d_slot, m->cos_t, m->sin_t, L->q, kv->k_pool,
-                                   kv->v_pool, T, s.hq, s.hkv, s.hd, l, kv->nb, st),
-                       "rope_append");
-            if (!ditems.empty())
+            if (!skip("norm")) cuda_check(rmsnorm(L->x, nullptr, ly.attn_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
+            if (skip("qkv")) {
+            } else if (fuse_qkv) {
+                // QKV GEMM with bias, RoPE and the paged K/V append fused into its epilogue
+                RopeEpi re{d_pos, d_slot, m->cos_t, m->sin_t, L->q, kv->k_pool, kv->v_pool,
+                           s.hq, s.hkv, s.hd, l, kv->nb};
+                linear(L, L->map_h, ly.qkv, T, EPI_QKV, nullptr, qd + 2 * kvd, ly.qkv_bias, nullptr, nullptr,
+                       -1, 0, nullptr, &re);
+            } else {
+                linear(L, L->map_h, ly.qkv, T, EPI_BF16, L->qkv, qd + 2 * kvd, ly.qkv_bias, nullptr, nullptr);
+                cuda_check(rope_append(L->qkv, d_pos, d_slot, m->cos_t, m->sin_t, L->q, kv->k_pool,
+                                       kv->v_pool, T, s.hq, s.hkv, s.hd, l, kv->nb, st),
+                           "rope_append");
+            }
+            if (!ditems.empty() && !skip("attn"))
                 L->timed(ASB_STAT_DECODE_ATTN, dattn_bytes, [&] {
                     cuda_check(decode_attention(kv->tk32, kv->tv32, L->q, d_ditems, int(ditems.size()),
                                                 max_ctx, d_tbl, L->attn, L->part_o, L->part_ml,
@@ -930,10 +948,10 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                                                  L->ppart_ml, as, st),
                                "prefill attention");
                 });
-            linear(L, L->map_attn, ly.o, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
-            cuda_check(rmsnorm(L->x, nullptr, ly.mlp_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
-            linear(L, L->map_h, ly.gate_up, T, EPI_SILU, L->act, s.ffn, nullptr, nullptr, nullptr);
-            linear(L, L->map_act, ly.down, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
+            if (!skip("o")) linear(L, L->map_attn, ly.o, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
+            if (!skip("norm")) cuda_check(rmsnorm(L->x, nullptr, ly.mlp_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
+            if (!skip("gate_up")) linear(L, L->map_h, ly.gate_up, T, EPI_SILU, L->act, s.ffn, nullptr, nullptr, nullptr);
+            if (!skip("down")) linear(L, L->map_act, ly.down, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
         }
         if (n_logit > 0) {
             // greedy sample fused into the LM head epilogue (swap path, <= 256 rows): the norm
