@@ -47,6 +47,19 @@ B200_PROFILE_SHAPE = {"total_sms": 144, "granularity": 16, "decode_max_rate": 40
                       "resume_max_rate": 120000.0, "resume_knee": 0.5}
 
 
+def profile_doc(api) -> tuple[str, str]:
+    """ProfileBundle for the controller: the B200 curves measured with our kernels on Green
+    Context partitions (paper_2603_10342_b200.profile_measure, committed under profiles/) when
+    present, else the hand-shaped fallback.  Returns (json text, source)."""
+    path = ROOT / "profiles" / f"b200_profile_{MODEL}.json"
+    if path.exists():
+        doc = json.loads(path.read_text())
+        doc.pop("measured", None)
+        return json.dumps(doc), f"measured ({path.relative_to(ROOT)})"
+    text, _ = api.profile_generate(B200_PROFILE_SHAPE)
+    return text, "shaped (B200_PROFILE_SHAPE)"
+
+
 def workload_config(n_gpus: int, rank: int, clock: str = "wall", policy: str = "agentserve",
                     profile_doc: str | None = None, profile_kernels: bool = False) -> dict:
     cfg = {
@@ -234,7 +247,7 @@ def run_mine(args) -> None:
         torch.cuda.set_device(local)
     from paper_2603_10342_b200.agsv import Agsv
     api = Agsv()
-    prof_doc, _ = api.profile_generate(B200_PROFILE_SHAPE)
+    prof_doc, prof_src = profile_doc(api)
     cfg = workload_config(n_gpus, rank, clock, args.policy, prof_doc)
     if clock == "wall":
         cfg["backend"]["device"] = int(os.environ.get("LOCAL_RANK", 0)) if os.environ.get("CUDA_VISIBLE_DEVICES") is None else 0
@@ -334,6 +347,7 @@ def run_mine(args) -> None:
                                "system prompt, 4x256-token tool outputs, 8-64-token decodes, 100 ms tools",
                    "agents_per_gpu": AGENTS_PER_GPU, "policy": args.policy, "clock": clock,
                    "parallelism": f"session-sharded replicas x{n_gpus} (no collective)",
+                   "profile": prof_src,
                    "l2": "weights (0.99 GB) and KV exceed the 126 MB L2; no flush needed"},
         "latency_ms": {"ttft": {"p50": _pct(ttft_all, 50), "p95": _pct(ttft_all, 95), "p99": _pct(ttft_all, 99)},
                        "tpot": {"p50": _pct(tpot_all, 50), "p95": _pct(tpot_all, 95), "p99": _pct(tpot_all, 99)},
@@ -392,7 +406,7 @@ def run_reference(args) -> None:
     from paper_2603_10342_b200.agsv import Agsv
     from tests.ref_oracle import REF_LIB
     api = Agsv(REF_LIB) if REF_LIB.exists() else Agsv()
-    prof_doc, _ = api.profile_generate(B200_PROFILE_SHAPE)
+    prof_doc, prof_src = profile_doc(api)
     cfg = workload_config(1, 0, "virtual", args.policy, prof_doc)
     td = tempfile.mkdtemp()
     tr = api.run(cfg)

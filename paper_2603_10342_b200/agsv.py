@@ -99,6 +99,10 @@ class Agsv:
         w = self._take(warn)
         return self._take(out), (w or None)
 
+    def profile_validate(self, doc: dict | str) -> None:
+        text = doc if isinstance(doc, str) else json.dumps(doc)
+        self._check(self.L.agsv_profile_validate(text.encode()))
+
 
 class Config:
     def __init__(self, api: Agsv, h):

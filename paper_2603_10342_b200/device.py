@@ -128,6 +128,13 @@ class Lane:
     def last_ms(self) -> float:
         return float(lib().asb_lane_last_ms(self.h))
 
+    def set_stream(self, stream) -> None:
+        check(lib().asb_lane_set_stream(self.h, stream))
+
+    def set_sms(self, sms: int) -> None:
+        """SM count the lane sizes its grids for (the partition its stream runs on)."""
+        check(lib().asb_lane_set_sms(self.h, sms))
+
     CATS = ("decode_attn", "prefill_attn", "decode_gemm", "prefill_gemm", "forward")
 
     def profile(self, on: bool = True) -> None:
@@ -145,6 +152,44 @@ class Lane:
     def close(self):
         if self.h:
             lib().asb_lane_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Slots:
+    """Green Context SM partitions (asb_slots_*): level l gives decode l*g SMs and prefill the
+    complement; level == levels() is the shared full device."""
+
+    def __init__(self, device: int = 0, levels: int = 9, granularity: int = 16):
+        h = C.c_void_p()
+        check(lib().asb_slots_create(device, levels, granularity, C.byref(h)))
+        self.h = h
+
+    def levels(self) -> int:
+        return lib().asb_slots_levels(self.h)
+
+    def green(self) -> bool:
+        return lib().asb_slots_green(self.h) == 1
+
+    def bind(self, level: int):
+        """(decode_stream, prefill_stream) raw cudaStream_t handles of one level."""
+        d, p = C.c_void_p(), C.c_void_p()
+        check(lib().asb_slots_bind(self.h, level, C.byref(d), C.byref(p)))
+        return d.value, p.value
+
+    def sm_counts(self, level: int) -> tuple[int, int]:
+        d, p = C.c_int(), C.c_int()
+        check(lib().asb_slots_sm_counts(self.h, level, C.byref(d), C.byref(p)))
+        return d.value, p.value
+
+    def close(self):
+        if self.h:
+            lib().asb_slots_free(self.h)
             self.h = None
 
     def __del__(self):
