@@ -25,19 +25,55 @@ namespace asb {
 namespace {
 
 // ============================================================================ prefill
-constexpr int kPThreads = 192;
-constexpr int kKvStages = 3;
+// Two GQA-packed query tiles per CTA (256 MMA rows = 2 x (128/G tokens) x G heads of one KV
+// head) share every K/V page.  Roles:
+//   warp 0     TMA producer (Q once, K/V pages into a ring)
+//   warp 1     MMA issuer: S_t = Q_t.K^T into TMEM, then O_t += P_t.V with P_t read straight
+//              from TMEM (the A-from-TMEM form of tcgen05.mma); S of page j+1 for both tiles is
+//              issued before P.V of page j, so the tensor core runs while softmax works.
+//   warps 2-5  softmax of tile 0, warps 6-9 softmax of tile 1: one query row per thread (its
+//              TMEM lane), P written back over its own S columns as packed bf16.
+// O accumulates in TMEM across pages.  The running max is refreshed lazily: O and l are
+// rescaled (in TMEM, by the row's own thread) only when a row max grows by more than 2^8, so
+// most pages never touch O outside the MMA.
+constexpr int kPThreads = 320;
+constexpr float kRescaleLog2 = 8.0f;
 
 template <int HD>
 struct PCfg {
     static constexpr int kHalves = HD / 64;
-    static constexpr int kQBytes = 128 * HD * 2;
+    static constexpr int kQTile = 128 * HD * 2;           // one 128-row Q tile
+    static constexpr int kQBytes = 2 * kQTile;
     static constexpr int kKBytes = kBlockTokens * HD * 2;
-    static constexpr int kStageBytes = 2 * kKBytes;  // K then V
-    static constexpr int kPBytes = 128 * kBlockTokens * 2;
-    static constexpr int kSmem = kQBytes + kKvStages * kStageBytes + kPBytes + 1024 + 256;
-    static constexpr int kTmemCols = 256;  // S0 | S1 | O (HD <= 128)
+    static constexpr int kStageBytes = 2 * kKBytes;       // K then V
+    static constexpr int kStages = HD == 128 ? 4 : 6;
+    static constexpr int kSmem = kQBytes + kStages * kStageBytes + 1024 + 256;
+    // TMEM: S[t][b] (64 fp32 cols each, P aliased as bf16 pairs) at (2t+b)*64, O[t] at 256+t*HD
+    static constexpr int kTmemCols = 512;
 };
+
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+        "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]),
+        "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]),
+        "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 template <int HD>
 __global__ void __launch_bounds__(kPThreads, 1)
@@ -54,34 +90,34 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
     uint8_t* sq = smem;
     uint8_t* skv = sq + C::kQBytes;
-    uint8_t* sp = skv + kKvStages * C::kStageBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sp + C::kPBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(skv + C::kStages * C::kStageBytes);
     uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;               // [kKvStages]
-    uint64_t* kv_empty = kv_full + kKvStages;   // [kKvStages]
-    uint64_t* s_full = kv_empty + kKvStages;    // [2]
-    uint64_t* s_free = s_full + 2;              // [2]
-    uint64_t* p_full = s_free + 2;
-    uint64_t* o_full = p_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+    uint64_t* kv_full = bars + 1;                 // [kStages]
+    uint64_t* kv_empty = kv_full + C::kStages;    // [kStages]
+    uint64_t* s_full = kv_empty + C::kStages;     // [2 tiles][2 bufs]
+    uint64_t* p_full = s_full + 4;                // [2][2]
+    uint64_t* pv_done = p_full + 4;               // [2][2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 4);
 
-    const PrefillItem it = items[blockIdx.x];
+    // heaviest items (most causal pages) first: they define the tail
+    const int item_idx = gridDim.x - 1 - blockIdx.x;
+    const PrefillItem it = items[item_idx];
     const int kvh = blockIdx.y;
     const int G = s.hq / s.hkv;
-    const int n_rows = it.n_q * G;  // valid MMA rows: (token, head-in-group)
+    const int tpt = 128 / G;          // tokens per tile
+    const int box_rows = tpt * G;     // valid MMA rows of a full tile
     const int total_blocks = (it.q_pos0 + it.n_q + kBlockTokens - 1) / kBlockTokens;
-    // split-KV (gridDim.z > 1): this CTA covers KV blocks [blk0, blk0 + n_kv_blocks)
     const int blk0 = blockIdx.z * blocks_per_split;
-    const int n_kv_blocks = max(0, min(total_blocks, blk0 + blocks_per_split) - blk0);
+    const int n_kv = max(0, min(total_blocks, blk0 + blocks_per_split) - blk0);
     const bool split = gridDim.z > 1;
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
-    if (n_kv_blocks == 0) {
-        // empty split: neutral partials for the valid rows
-        const size_t base = (static_cast<size_t>(blockIdx.x) * gridDim.y + kvh) * gridDim.z + blockIdx.z;
-        for (int r = threadIdx.x; r < n_rows; r += blockDim.x) {
-            part_ml[(base * 128 + r) * 2 + 0] = -FLT_MAX;
-            part_ml[(base * 128 + r) * 2 + 1] = 0.f;
+    const size_t pbase = (static_cast<size_t>(item_idx) * gridDim.y + kvh) * gridDim.z + blockIdx.z;
+    if (n_kv == 0) {
+        // empty split: neutral partials
+        for (int r = threadIdx.x; r < 256; r += blockDim.x) {
+            part_ml[(pbase * 256 + r) * 2 + 0] = -FLT_MAX;
+            part_ml[(pbase * 256 + r) * 2 + 1] = 0.f;
         }
         return;
     }
@@ -91,222 +127,233 @@ __global__ void __launch_bounds__(kPThreads, 1)
         tma_prefetch_desc(&tmap_k);
         tma_prefetch_desc(&tmap_v);
         mbar_init(q_full, 1);
-        for (int i = 0; i < kKvStages; ++i) {
+        for (int i = 0; i < C::kStages; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 4; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&s_free[i], 128);
+            mbar_init(&p_full[i], 128);
+            mbar_init(&pv_done[i], 1);
         }
-        mbar_init(p_full, 128);
-        mbar_init(o_full, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
-    // The Q box covers (128 / G) * G rows; the remaining (< G) rows stay zero so their
-    // (discarded) outputs are finite.
-    const int box_rows = (128 / G) * G;
-    for (int i = threadIdx.x; i < C::kHalves * (128 - box_rows) * 8; i += blockDim.x) {
-        const int h = i / ((128 - box_rows) * 8), rem = i % ((128 - box_rows) * 8);
-        reinterpret_cast<uint4*>(sq + h * (128 * 128) + (box_rows + rem / 8) * 128)[rem % 8] = make_uint4(0, 0, 0, 0);
+    // rows of a tile beyond box_rows (< G of them) are never loaded: zero them once
+    for (int i = threadIdx.x; i < 2 * C::kHalves * (128 - box_rows) * 8; i += blockDim.x) {
+        const int per_t = C::kHalves * (128 - box_rows) * 8;
+        const int t = i / per_t, j = i % per_t;
+        const int h = j / ((128 - box_rows) * 8), rem = j % ((128 - box_rows) * 8);
+        reinterpret_cast<uint4*>(sq + t * C::kQTile + h * (128 * 128) + (box_rows + rem / 8) * 128)[rem % 8] =
+            make_uint4(0, 0, 0, 0);
     }
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
     pdl_trigger();
     pdl_wait();  // q / K / V were written by the kernels before us
+    const uint32_t tmem = *tmem_slot;
     const int32_t* table = tables + it.table_off;
 
     if (warp == 0) {
         if (elect_one()) {
-            mbar_expect_tx(q_full, C::kHalves * box_rows * 128);  // full box, incl. OOB fill
+            mbar_expect_tx(q_full, 2 * C::kHalves * box_rows * 128);  // full boxes incl. OOB fill
 #pragma unroll
-            for (int h = 0; h < C::kHalves; ++h)
-                tma_load_3d(sq + h * (128 * 128), &tmap_q, q_full, h * 64, kvh * G, it.q_row0);
-            const uint64_t pol = policy_evict_last();  // K/V blocks are re-read by other heads
-            for (int j = 0; j < n_kv_blocks; ++j) {
-                const int st = j % kKvStages;
-                const uint32_t ph = (j / kKvStages) & 1;
-                mbar_wait(&kv_empty[st], ph ^ 1);
+            for (int t = 0; t < 2; ++t)
+#pragma unroll
+                for (int h = 0; h < C::kHalves; ++h)
+                    tma_load_3d(sq + t * C::kQTile + h * (128 * 128), &tmap_q, q_full, h * 64, kvh * G,
+                                it.q_row0 + t * tpt);
+            const uint64_t pol = policy_evict_last();  // pages are re-read by the other heads
+            for (int j = 0; j < n_kv; ++j) {
+                const int st = j % C::kStages;
+                mbar_wait(&kv_empty[st], ((j / C::kStages) & 1) ^ 1);
                 mbar_expect_tx(&kv_full[st], C::kStageBytes);
                 const int blk = table[blk0 + j];
-                const int row =
-                    ((s.layer * s.num_blocks + blk) * s.hkv + kvh) * kBlockTokens;
+                const int row = ((s.layer * s.num_blocks + blk) * s.hkv + kvh) * kBlockTokens;
                 uint8_t* kdst = skv + st * C::kStageBytes;
                 uint8_t* vdst = kdst + C::kKBytes;
 #pragma unroll
                 for (int h = 0; h < C::kHalves; ++h) {
-                    tma_load_2d_hint(kdst + h * (kBlockTokens * 128), &tmap_k, &kv_full[st],
-                                     h * 64, row, pol);
-                    tma_load_2d_hint(vdst + h * (kBlockTokens * 128), &tmap_v, &kv_full[st],
-                                     h * 64, row, pol);
+                    tma_load_2d_hint(kdst + h * (kBlockTokens * 128), &tmap_k, &kv_full[st], h * 64, row, pol);
+                    tma_load_2d_hint(vdst + h * (kBlockTokens * 128), &tmap_v, &kv_full[st], h * 64, row, pol);
                 }
             }
         }
-        __syncwarp();  // reconverge before the CTA barrier
+        __syncwarp();
     } else if (warp == 1) {
         constexpr uint32_t idesc_s = make_idesc_bf16(128, kBlockTokens, false, false);
         constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
-        const uint32_t q_addr = smem_u32(sq);
-        const uint32_t p_addr = smem_u32(sp);
         mbar_wait(q_full, 0);
-        auto issue_s = [&](int j) {
-            const int st = j % kKvStages;
-            const int sb = j & 1;
-            mbar_wait(&kv_full[st], (j / kKvStages) & 1);
-            if (j >= 2) mbar_wait(&s_free[sb], ((j - 2) >> 1) & 1);
+        auto issue_s = [&](int t, int j) {
+            const int st = j % C::kStages, b = j & 1;
+            if (j >= 2) mbar_wait(&pv_done[2 * t + b], ((j >> 1) - 1) & 1);  // P_t(j-2) consumed
             tc_fence_after();
             if (elect_one()) {
+                const uint32_t q_addr = smem_u32(sq + t * C::kQTile);
                 const uint32_t k_addr = smem_u32(skv + st * C::kStageBytes);
 #pragma unroll
                 for (int k = 0; k < HD / 16; ++k) {
                     const int h = k / 4, kk = k % 4;
                     const uint64_t ad = make_sw128_desc(q_addr + h * 16384 + kk * 32, 16, 1024);
-                    const uint64_t bd =
-                        make_sw128_desc(k_addr + h * (kBlockTokens * 128) + kk * 32, 16, 1024);
-                    umma_bf16(tmem + sb * kBlockTokens, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+                    const uint64_t bd = make_sw128_desc(k_addr + h * (kBlockTokens * 128) + kk * 32, 16, 1024);
+                    umma_bf16(tmem + (2 * t + b) * 64, ad, bd, idesc_s, k > 0 ? 1u : 0u);
                 }
-                umma_commit(&s_full[sb]);
+                umma_commit(&s_full[2 * t + b]);
             }
             __syncwarp();
         };
-        auto issue_pv = [&](int j) {
-            const int st = j % kKvStages;
-            mbar_wait(p_full, j & 1);
+        auto issue_pv = [&](int t, int j) {
+            const int st = j % C::kStages, b = j & 1;
+            mbar_wait(&p_full[2 * t + b], (j >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t v_addr = smem_u32(skv + st * C::kStageBytes + C::kKBytes);
 #pragma unroll
                 for (int k = 0; k < kBlockTokens / 16; ++k) {
-                    const uint64_t ad = make_sw128_desc(p_addr + k * 32, 16, 1024);
                     // V is MN-major (head_dim contiguous): LBO = distance between 64-wide
                     // head_dim atoms, SBO = 8 key rows; 16 keys per MMA = 2048 bytes.
-                    const uint64_t bd =
-                        make_sw128_desc(v_addr + k * 2048, kBlockTokens * 128, 1024);
-                    umma_bf16(tmem + 2 * kBlockTokens, ad, bd, idesc_o, k > 0 ? 1u : 0u);
+                    const uint64_t bd = make_sw128_desc(v_addr + k * 2048, kBlockTokens * 128, 1024);
+                    umma_bf16_ts(tmem + 256 + t * HD, tmem + (2 * t + b) * 64 + 8 * k, bd, idesc_o,
+                                 (j > 0 || k > 0) ? 1u : 0u);
                 }
-                umma_commit(o_full);
-                umma_commit(&kv_empty[st]);
+                umma_commit(&pv_done[2 * t + b]);
+                if (t == 1) umma_commit(&kv_empty[st]);
             }
             __syncwarp();
         };
-        issue_s(0);
-        for (int j = 1; j < n_kv_blocks; ++j) {
-            issue_s(j);
-            issue_pv(j - 1);
+        auto wait_kv = [&](int j) {
+            mbar_wait(&kv_full[j % C::kStages], (j / C::kStages) & 1);
+        };
+        wait_kv(0);
+        issue_s(0, 0);
+        issue_s(1, 0);
+        for (int j = 0; j < n_kv; ++j) {
+            if (j + 1 < n_kv) {
+                wait_kv(j + 1);
+                issue_s(0, j + 1);
+                issue_s(1, j + 1);
+            }
+            issue_pv(0, j);
+            issue_pv(1, j);
         }
-        issue_pv(n_kv_blocks - 1);
     } else {
-        // Softmax / correction warps: one query row per thread.
+        // softmax: tile t, one query row per thread (TMEM lane quarter = warp % 4)
+        const int t = (warp - 2) / 4;
         const uint32_t quarter = warp & 3;
-        const int r = quarter * 32 + lane;
-        const int qpos = it.q_pos0 + r / G;  // row r = (token r / G, head kvh*G + r % G)
+        const int rr = quarter * 32 + lane;             // row within the tile
+        const int tok = t * tpt + rr / G;               // token within the item
+        const bool valid = rr < box_rows && tok < it.n_q;
+        const int qpos = it.q_pos0 + tok;
         const uint32_t t_lane = tmem + ((quarter * 32u) << 16);
-        float o[HD];
-#pragma unroll
-        for (int d = 0; d < HD; ++d) o[d] = 0.f;
-        float m_run = -FLT_MAX, l_run = 0.f, alpha_prev = 1.f;
-        uint8_t* prow = sp + r * 128;
-        for (int j = 0; j < n_kv_blocks; ++j) {
-            const int sb = j & 1;
-            mbar_wait(&s_full[sb], (j >> 1) & 1);
+        const uint32_t o_col = t_lane + 256 + t * HD;
+        float m_ref = -FLT_MAX, l_run = 0.f;
+        for (int j = 0; j < n_kv; ++j) {
+            const int b = j & 1;
+            const uint32_t s_col = t_lane + (2 * t + b) * 64;
+            mbar_wait(&s_full[2 * t + b], (j >> 1) & 1);
             tc_fence_after();
             uint32_t sa[32], sb2[32];
-            tmem_ld32(t_lane + sb * kBlockTokens, sa);
-            tmem_ld32(t_lane + sb * kBlockTokens + 32, sb2);
+            tmem_ld32(s_col, sa);
+            tmem_ld32(s_col + 32, sb2);
             tmem_ld_wait();
-            tc_fence_before();
-            mbar_arrive(&s_free[sb]);
-            // mask + scale (log2 domain)
             const int kbase = (blk0 + j) * kBlockTokens;
-            float mx = m_run;
-            float sv[64];
+            const bool full_vis = kbase + kBlockTokens - 1 <= qpos;
+            float mx = -FLT_MAX;
 #pragma unroll
             for (int c = 0; c < 64; ++c) {
-                const float x = __uint_as_float(c < 32 ? sa[c] : sb2[c - 32]) * s.scale_log2;
-                sv[c] = (kbase + c <= qpos) ? x : -FLT_MAX;
-                mx = fmaxf(mx, sv[c]);
+                const float x = __uint_as_float(c < 32 ? sa[c] : sb2[c - 32]);
+                if (full_vis || kbase + c <= qpos) mx = fmaxf(mx, x);
             }
-            const float alpha = exp2f(m_run - mx);
+            mx = mx == -FLT_MAX ? -FLT_MAX : mx * s.scale_log2;
+            const bool need = mx > m_ref + kRescaleLog2;
+            if (__any_sync(0xffffffffu, need)) {
+                const float alpha = need ? exp2f(m_ref - mx) : 1.f;
+                if (j > 0) {
+                    // O_t holds P.V of pages < j: wait for the last of them, rescale in place
+                    mbar_wait(&pv_done[2 * t + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int c = 0; c < HD; c += 32) {
+                        uint32_t ov[32];
+                        tmem_ld32(o_col + c, ov);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+                        tmem_st32(o_col + c, ov);
+                    }
+                    tmem_st_wait();
+                }
+                if (need) {
+                    l_run *= alpha;
+                    m_ref = mx;
+                }
+            }
+            const float nm = -m_ref;
             float psum = 0.f;
             uint32_t pk[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
-                const float p0 = (kbase + 2 * c <= qpos) ? exp2f(sv[2 * c] - mx) : 0.f;
-                const float p1 = (kbase + 2 * c + 1 <= qpos) ? exp2f(sv[2 * c + 1] - mx) : 0.f;
-                const uint32_t packed = pack_bf16(p0, p1);
-                // accumulate the rounded probabilities so l matches what P.V sums
-                psum += bf16_lo(packed) + bf16_hi(packed);
-                pk[c] = packed;
-            }
-            l_run = l_run * alpha + psum;
-            m_run = mx;
-            if (j >= 1) {
-                // fold in P_{j-1}.V_{j-1}
-                mbar_wait(o_full, (j - 1) & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int c = 0; c < HD; c += 32) {
-                    uint32_t ov[32];
-                    tmem_ld32(t_lane + 2 * kBlockTokens + c, ov);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        o[c + e] = o[c + e] * alpha_prev + __uint_as_float(ov[e]);
+                const float x0 = __uint_as_float(c < 16 ? sa[2 * c] : sb2[2 * c - 32]);
+                const float x1 = __uint_as_float(c < 16 ? sa[2 * c + 1] : sb2[2 * c + 1 - 32]);
+                float p0 = exp2f(fmaf(x0, s.scale_log2, nm));
+                float p1 = exp2f(fmaf(x1, s.scale_log2, nm));
+                if (!full_vis) {
+                    p0 = (kbase + 2 * c <= qpos) ? p0 : 0.f;
+                    p1 = (kbase + 2 * c + 1 <= qpos) ? p1 : 0.f;
                 }
-                tc_fence_before();
+                psum += p0 + p1;
+                pk[c] = pack_bf16(p0, p1);
             }
-            alpha_prev = alpha;
-            // P row -> smem (K-major SWIZZLE_128B: chunk c of row r at (c ^ (r & 7)))
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                uint4 v;
-                v.x = pk[4 * c + 0];
-                v.y = pk[4 * c + 1];
-                v.z = pk[4 * c + 2];
-                v.w = pk[4 * c + 3];
-                *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) * 16)) = v;
-            }
-            fence_proxy_async_smem();
-            mbar_arrive(p_full);
+            l_run += psum;
+            tmem_st32(s_col, pk);  // P over its own S columns (A operand of P.V)
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&p_full[2 * t + b]);
         }
-        mbar_wait(o_full, (n_kv_blocks - 1) & 1);
+        mbar_wait(&pv_done[2 * t + ((n_kv - 1) & 1)], ((n_kv - 1) >> 1) & 1);
         tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < HD; c += 32) {
-            uint32_t ov[32];
-            tmem_ld32(t_lane + 2 * kBlockTokens + c, ov);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[c + e] = o[c + e] * alpha_prev + __uint_as_float(ov[e]);
-        }
-        tc_fence_before();
+        const int prow = t * 128 + rr;
         if (split) {
-            if (r < n_rows) {
-                const size_t base =
-                    ((static_cast<size_t>(blockIdx.x) * gridDim.y + kvh) * gridDim.z + blockIdx.z) * 128 + r;
-                float4* po = reinterpret_cast<float4*>(part_o + base * HD);
+            const size_t base = pbase * 256 + prow;
+            float4* po = reinterpret_cast<float4*>(part_o + base * HD);
+#pragma unroll 1
+            for (int c = 0; c < HD; c += 32) {
+                uint32_t ov[32];
+                tmem_ld32(o_col + c, ov);
+                tmem_ld_wait();
+                if (valid) {
 #pragma unroll
-                for (int c = 0; c < HD / 4; ++c)
-                    po[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
-                part_ml[base * 2 + 0] = m_run;
+                    for (int e = 0; e < 8; ++e)
+                        po[c / 4 + e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                                                    __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
+                }
+            }
+            if (valid) {
+                part_ml[base * 2 + 0] = m_ref;
                 part_ml[base * 2 + 1] = l_run;
             }
-        } else if (r < n_rows) {
+        } else {
             const float inv = 1.f / l_run;
             uint4* dst = reinterpret_cast<uint4*>(
-                out + static_cast<size_t>(it.q_row0 + r / G) * (s.hq * HD) + (kvh * G + r % G) * HD);
+                out + static_cast<size_t>(it.q_row0 + tok) * (s.hq * HD) + (kvh * G + rr % G) * HD);
+#pragma unroll 1
+            for (int c = 0; c < HD; c += 32) {
+                uint32_t ov[32];
+                tmem_ld32(o_col + c, ov);
+                tmem_ld_wait();
+                if (valid) {
 #pragma unroll
-            for (int c = 0; c < HD / 8; ++c) {
-                uint4 v;
-                v.x = pack_bf16(o[8 * c + 0] * inv, o[8 * c + 1] * inv);
-                v.y = pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
-                v.z = pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
-                v.w = pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
-                dst[c] = v;
+                    for (int e = 0; e < 4; ++e) {
+                        uint4 v;
+                        v.x = pack_bf16(__uint_as_float(ov[8 * e + 0]) * inv, __uint_as_float(ov[8 * e + 1]) * inv);
+                        v.y = pack_bf16(__uint_as_float(ov[8 * e + 2]) * inv, __uint_as_float(ov[8 * e + 3]) * inv);
+                        v.z = pack_bf16(__uint_as_float(ov[8 * e + 4]) * inv, __uint_as_float(ov[8 * e + 5]) * inv);
+                        v.w = pack_bf16(__uint_as_float(ov[8 * e + 6]) * inv, __uint_as_float(ov[8 * e + 7]) * inv);
+                        dst[c / 8 + e] = v;
+                    }
+                }
             }
         }
     }
@@ -318,7 +365,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
 }
 
-// Merge split-KV partials of prefill rows.  grid = (n_items, hkv, 128 rows), block = HD.
+// Merge split-KV partials of prefill rows.  grid = (n_items, hkv, 256 rows), block = HD.
 template <int HD>
 __global__ void prefill_combine_kernel(const PrefillItem* __restrict__ items,
                                        const float* __restrict__ part_o,
@@ -326,23 +373,27 @@ __global__ void prefill_combine_kernel(const PrefillItem* __restrict__ items,
                                        __nv_bfloat16* __restrict__ out, int hq, int hkv) {
     pdl_trigger();
     pdl_wait();
-    const PrefillItem it = items[blockIdx.x];
+    const int item_idx = gridDim.x - 1 - blockIdx.x;  // same item order as the attention grid
+    const PrefillItem it = items[item_idx];
     const int G = hq / hkv;
-    const int r = blockIdx.z, kvh = blockIdx.y, d = threadIdx.x;
-    if (r >= it.n_q * G) return;
-    const size_t base = (static_cast<size_t>(blockIdx.x) * hkv + kvh) * splits;
+    const int tpt = 128 / G;
+    const int prow = blockIdx.z, kvh = blockIdx.y, d = threadIdx.x;
+    const int t = prow / 128, rr = prow % 128;
+    const int tok = t * tpt + rr / G;
+    if (rr >= tpt * G || tok >= it.n_q) return;
+    const size_t base = (static_cast<size_t>(item_idx) * hkv + kvh) * splits;
     float m = -FLT_MAX;
-    for (int sp = 0; sp < splits; ++sp) m = fmaxf(m, part_ml[((base + sp) * 128 + r) * 2]);
+    for (int sp = 0; sp < splits; ++sp) m = fmaxf(m, part_ml[((base + sp) * 256 + prow) * 2]);
     float l = 0.f, o = 0.f;
     for (int sp = 0; sp < splits; ++sp) {
-        const size_t row = (base + sp) * 128 + r;
+        const size_t row = (base + sp) * 256 + prow;
         const float ls = part_ml[row * 2 + 1];
         if (ls == 0.f) continue;
         const float w = exp2f(part_ml[row * 2] - m);
         l += ls * w;
         o += part_o[row * HD + d] * w;
     }
-    out[static_cast<size_t>(it.q_row0 + r / G) * hq * HD + (kvh * G + r % G) * HD + d] =
+    out[static_cast<size_t>(it.q_row0 + tok) * hq * HD + (kvh * G + rr % G) * HD + d] =
         __float2bfloat16_rn(o / l);
 }
 
@@ -365,7 +416,7 @@ cudaError_t prefill_launch(const CUtensorMap& tq, const CUtensorMap& tk, const C
     cudaError_t e = launch_k(prefill_attention_kernel<HD>, grid, dim3(kPThreads), C::kSmem, stream, tq, tk, tv,
                              items, tables, out, part_o, part_ml, bps, s);
     if (e == cudaSuccess && splits > 1)
-        e = launch_k(prefill_combine_kernel<HD>, dim3(n_items, s.hkv, 128), dim3(HD), 0, stream, items,
+        e = launch_k(prefill_combine_kernel<HD>, dim3(n_items, s.hkv, 256), dim3(HD), 0, stream, items,
                      static_cast<const float*>(part_o), static_cast<const float*>(part_ml), splits, out, s.hq,
                      s.hkv);
     return e;
@@ -374,6 +425,7 @@ cudaError_t prefill_launch(const CUtensorMap& tq, const CUtensorMap& tk, const C
 }  // namespace
 
 int prefill_tokens_per_tile(int hq, int hkv) { return 128 / (hq / hkv); }
+int prefill_tokens_per_cta(int hq, int hkv) { return 2 * prefill_tokens_per_tile(hq, hkv); }
 
 int prefill_splits(int n_items, int hkv, int max_blocks, int num_sms, size_t ws_rows) {
     // split the KV range only when the (item, kv head) grid leaves SMs idle
@@ -381,7 +433,7 @@ int prefill_splits(int n_items, int hkv, int max_blocks, int num_sms, size_t ws_
     int splits = (2 * num_sms + ctas - 1) / ctas;
     splits = std::min(splits, std::max(1, max_blocks / 2));
     splits = std::min(splits, 32);
-    while (splits > 1 && static_cast<size_t>(ctas) * splits * 128 > ws_rows) --splits;
+    while (splits > 1 && static_cast<size_t>(ctas) * splits * 256 > ws_rows) --splits;
     return std::max(splits, 1);
 }
 

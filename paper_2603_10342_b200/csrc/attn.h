@@ -13,12 +13,13 @@ namespace asb {
 // a single TMA box for prefill attention and a 128-bit-coalesced stream for decode.
 constexpr int kBlockTokens = 64;
 
-// One prefill-attention work item: up to prefill_tokens_per_tile() query tokens of one
-// segment; the CTA's 128 MMA rows are those tokens x the G query heads of one KV head.
+// One prefill-attention work item: up to prefill_tokens_per_cta() query tokens of one
+// segment; the CTA's 2 x 128 MMA rows are those tokens x the G query heads of one KV head
+// (two Q tiles of prefill_tokens_per_tile() tokens each).
 struct PrefillItem {
     int q_row0;     // first token row in the q / out buffers
     int q_pos0;     // absolute position of that token
-    int n_q;        // valid query tokens (<= 128 / G)
+    int n_q;        // valid query tokens (<= 2 * 128 / G)
     int table_off;  // offset of this segment's block table in the batch table array
 };
 
@@ -38,9 +39,10 @@ struct AttnShape {
 };
 
 // grid = (items, hkv, splits).  Split-KV over gridDim.z when the grid is small (resume
-// chunks): partials part_o [items*hkv*splits*128][hd] fp32 and part_ml [..][2], merged by a
+// chunks): partials part_o [items*hkv*splits*256][hd] fp32 and part_ml [..][2], merged by a
 // combine kernel.  tmap_q is the 3-D map [T][hq][hd] with box [tokens_per_tile][G][64].
 int prefill_tokens_per_tile(int hq, int hkv);
+int prefill_tokens_per_cta(int hq, int hkv);
 int prefill_splits(int n_items, int hkv, int max_blocks, int num_sms, size_t ws_rows);
 cudaError_t prefill_attention(const CUtensorMap& tmap_q, const CUtensorMap& tmap_k,
                               const CUtensorMap& tmap_v, const PrefillItem* items, int n_items,

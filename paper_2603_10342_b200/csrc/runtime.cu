@@ -742,7 +742,7 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->part_ml = static_cast<float*>(
             dmalloc(size_t(dec_rows) * s.hq * L->max_splits * 2 * 4, L->allocs));
         // split-KV partials for small prefill grids (resume chunks): <= 4096 rows of 128 queries
-        L->ppart_rows = size_t(4096) * 128 / 16;
+        L->ppart_rows = size_t(4096) * 256 / 16;
         L->ppart_o = static_cast<float*>(dmalloc(L->ppart_rows * s.hd * 4, L->allocs));
         L->ppart_ml = static_cast<float*>(dmalloc(L->ppart_rows * 2 * 4, L->allocs));
         L->meta_ints = size_t(3) * T + L->max_segs + L->max_tbl + 4 * size_t(L->max_segs) +
@@ -851,7 +851,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                 ditems.push_back(DecodeItem{row, start + 1, toff, 0});
                 max_ctx = std::max(max_ctx, start + 1);
             } else {
-                const int tpt = prefill_tokens_per_tile(s.hq, s.hkv);
+                const int tpt = prefill_tokens_per_cta(s.hq, s.hkv);
                 for (int q0 = 0; q0 < g.n_tokens; q0 += tpt)
                     pitems.push_back(PrefillItem{row + q0, start + q0, std::min(tpt, g.n_tokens - q0), toff});
                 max_pblocks = std::max(max_pblocks, (start + g.n_tokens + kBlockTokens - 1) / kBlockTokens);
