@@ -155,42 +155,47 @@ def _episode_stats(recs: list[dict]) -> dict:
             "batch_sizes": [s["batch"] for s in steps]}
 
 
+_ORACLE = {}
+
+
 def _cpu_baseline(tmpl_stats: dict, budget_s: float = 20.0) -> dict:
     """CPU fp32 oracle forward on the host cores, on a bounded sample of the same workload:
-    one 256-token prefill unit and a few 8-row decode steps (8 sessions x 1 token, context 256)
-    timed with all OpenMP threads, then extrapolated to the episode's measured work
-    (prefill tokens and decode steps counted from the GPU episode's trace).  The short
-    sampled context under-counts CPU attention work, so this is an upper bound on CPU
-    throughput."""
+    one 128-token prefill and a few 8-row decode steps (8 sessions x 1 token on short
+    contexts) timed with all OpenMP threads, then extrapolated to the episode's measured work
+    (prefill tokens and decode steps counted from the episode's trace).  The short sampled
+    contexts under-count CPU attention work, so this is an upper bound on CPU throughput."""
     import numpy as np
     from oracle.forward import OracleModel, token_stream
     t0 = time.perf_counter()
-    om = OracleModel(MODEL, seed=13, max_ctx=512)
+    if MODEL not in _ORACLE:
+        _ORACLE[MODEL] = OracleModel(MODEL, seed=13, max_ctx=512)
+    om = _ORACLE[MODEL]
     build_s = time.perf_counter() - t0
     V = om.spec.vocab
     sess = [om.session() for _ in range(AGENTS_PER_GPU)]
+    n_pf = 128
     t0 = time.perf_counter()
-    sess[0].forward(token_stream(13, "tok/0/cold", 256, V))
+    sess[0].forward(token_stream(13, "tok/0/cold", n_pf, V))
     prefill_s = time.perf_counter() - t0
     for i in range(1, AGENTS_PER_GPU):
-        sess[i].forward(token_stream(13, f"tok/{i}/cold", 256, V))
+        sess[i].forward(token_stream(13, f"tok/{i}/cold", 32, V))
     steps, step_s = 0, 0.0
     deadline = time.perf_counter() + budget_s
-    while steps < 3 and time.perf_counter() < deadline:
+    while steps < 2 and time.perf_counter() < deadline:
         t0 = time.perf_counter()
         for s in sess:
             s.forward(np.array([1 + steps], dtype=np.int32))
         step_s += time.perf_counter() - t0
         steps += 1
     per_step = step_s / max(steps, 1)  # 8 rows
-    per_prefill_tok = prefill_s / 256.0
+    per_prefill_tok = prefill_s / float(n_pf)
     ep = tmpl_stats
     t_cpu = (ep["prefill_tokens"] + ep["chunk_tokens"]) * per_prefill_tok + \
         ep["n_steps"] * per_step * (np.mean(ep["batch_sizes"]) / AGENTS_PER_GPU if ep["batch_sizes"] else 1.0)
     return {"value": ep["tokens"] / t_cpu if t_cpu > 0 else 0.0, "unit": "tokens/s",
             "cores": os.cpu_count(), "kind": "port",
-            "sample": (f"CPU fp32 oracle ({MODEL}, OpenMP {os.cpu_count()} threads): 256-token prefill "
-                       f"{prefill_s:.2f}s, {steps} decode steps x {AGENTS_PER_GPU} rows @ctx 256 "
+            "sample": (f"CPU fp32 oracle ({MODEL}, OpenMP {os.cpu_count()} threads): {n_pf}-token prefill "
+                       f"{prefill_s:.2f}s, {steps} decode steps x {AGENTS_PER_GPU} rows @ctx <=130 "
                        f"{per_step:.2f}s/step (weights built in {build_s:.1f}s); extrapolated to the "
                        f"episode's {ep['prefill_tokens'] + ep['chunk_tokens']} prefill tokens and "
                        f"{ep['n_steps']} decode steps")}
@@ -387,6 +392,7 @@ def run_mine(args) -> None:
                                "unit": "GB/s" if v["unit"] == "bytes" else "TFLOP/s"}
                            for k, v in kern.items()}
     if n_gpus == 1 and not args.no_cpu:
+        _cpu_baseline(stats[0], budget_s=5.0)  # warm the OpenMP pool and the weights' pages
         line["cpu_baseline"] = _cpu_baseline(stats[0])
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -412,16 +418,18 @@ def run_reference(args) -> None:
     tr = api.run(cfg)
     recs = [json.loads(x) for x in tr.jsonl(td).splitlines()]
     st = _episode_stats(recs)
+    for _ in range(args.warmup):
+        _cpu_baseline(st, budget_s=10.0)
     vals = []
     base = None
     t0 = time.perf_counter()
-    for _ in range(max(1, min(args.steps, 2))):
-        base = _cpu_baseline(st, budget_s=15.0)
+    for _ in range(args.steps):
+        base = _cpu_baseline(st, budget_s=10.0)
         vals.append(base["value"])
     wall = time.perf_counter() - t0
     v = sum(vals) / len(vals)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s",
-            "n_gpus": n, "steps": len(vals), "warmup": 0, "ms_per_step": round(1000 * wall / len(vals), 1),
+            "n_gpus": n, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * wall / len(vals), 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": f"C2 episode ({MODEL}, {AGENTS_PER_GPU} agents) "
                                                         "on the CPU fp32 oracle forward"},
