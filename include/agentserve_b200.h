@@ -130,7 +130,8 @@ enum {
     ASB_STAT_DECODE_GEMM = 2,  /* units: weight + activation bytes (swap-AB path) */
     ASB_STAT_PREFILL_GEMM = 3, /* units: FLOPs */
     ASB_STAT_FORWARD = 4,      /* whole forward; units: tokens */
-    ASB_STAT_COUNT = 5
+    ASB_STAT_DECODE_STEP = 5,  /* persistent decode-step kernel; units: weight + K/V bytes */
+    ASB_STAT_COUNT = 6
 };
 asb_status asb_lane_profile(asb_lane* lane, int enable);
 /* SMs available to the lane's current stream (green-context partition); sizes persistent
@@ -164,13 +165,24 @@ asb_status asb_slots_sm_counts(const asb_slots* s, int decode_level, int* decode
 
 /* --- debug / test hooks (used by tests/, not by the engine) --------------------------------*/
 /* Y[tokens][n_out] = X[tokens][k] . W[n_out][k]^T on device pointers; epi: 0 bf16(+bias),
- * 1 +resid, 2 silu-mul (interleaved rows), 3 fp32.  force_path: -1 auto, 0 normal, 1 swap. */
+ * 1 +resid, 2 silu-mul (interleaved rows), 3 fp32.  force_path: -1 auto, 0 normal, 1 swap,
+ * 2 small-batch dgemv (tokens <= 32). */
 /* ASB_GEMM_TIMELINE=1: per-CTA globaltimer stamps (start, MMA done, epilogue done, exit) of the
  * lane's most recent GEMM launch, [148][4] ns. */
 asb_status asb_debug_gemm_timeline(asb_lane* lane, unsigned long long* out, int n);
+/* ASB_MK_TIMELINE=1 at lane creation: globaltimer (ns) at the start of every phase of the
+ * lane's most recent persistent decode-step launch, [num_sms][256] (slot 255 = CTA exit). */
+asb_status asb_debug_mk_timeline(asb_lane* lane, unsigned long long* out, int n);
 asb_status asb_debug_gemm(const void* x, const void* w, const void* bias, const void* resid,
                           void* out, int tokens, int n_out, int k, int epi, int force_path,
                           int splits, void* stream);
+/* Average device time of `reps` back-to-back launches of one linear layer (weights packed
+ * once into copies that exceed L2, PDL on); force_path 2 = small-batch dgemv.  stream: e.g. a
+ * green-context stream from asb_slots_bind (NULL: a new full-device stream); num_sms: the SMs
+ * that stream owns (0: the whole device). */
+asb_status asb_debug_gemm_bench(const void* x, const void* w, void* out, int tokens, int n_out, int k,
+                                int epi, int force_path, int reps, int num_sms, void* stream,
+                                float* us_per_launch);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

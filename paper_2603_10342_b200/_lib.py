@@ -83,9 +83,11 @@ SIGNATURES = {
     "asb_slots_bind": (I, [P, I, PP, PP]),
     "asb_slots_sm_counts": (I, [P, I, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "asb_debug_gemm": (I, [P, P, P, P, P, I, I, I, I, I, I, P]),
+    "asb_debug_gemm_bench": (I, [P, P, P, I, I, I, I, I, I, I, P, FP]),
     "asb_lane_profile": (I, [P, I]),
     "asb_lane_stats": (I, [P, I, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64), I]),
     "asb_lane_set_sms": (I, [P, I]),
+    "asb_debug_mk_timeline": (I, [P, C.POINTER(C.c_ulonglong), I]),
     "asb_lane_counters": (I, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64), I]),
 }
 

@@ -28,6 +28,7 @@
 #include "attn.h"
 #include "launch.cuh"
 #include "sm100.cuh"
+#include "warpmma.cuh"
 
 namespace asb {
 
@@ -49,40 +50,6 @@ struct DC {
     static constexpr int kRing = kStages * kStage;
 };
 
-__device__ __forceinline__ void named_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
-                                        uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
-                                          uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-// D = A (16x16 bf16, row) * B (16x8 bf16, col) + D, fp32 accumulate
-__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
-                                         uint32_t a3, uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-        "{%8,%9}, {%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-// byte offset of 16-byte chunk `c` (0..HD/8-1) of row `r` in a [rows][HD] tile stored as
-// HD/64 SWIZZLE_128B boxes of [kSub rows][64 cols]
-template <int HD>
-__device__ __forceinline__ uint32_t sw_off(int r, int c) {
-    const int box = c >> 3, cc = c & 7;
-    return box * (kSub * 128) + r * 128 + ((cc ^ (r & 7)) << 4);
-}
-
 // Stage of item i.  Item i is consumed by warp i % W; giving every warp its own S / W stages
 // (visited in order) means each mbarrier has exactly one waiter that waits its phases
 // strictly in sequence — with round-robin consumers sharing a ring, a fast warp could wait
@@ -96,8 +63,8 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                        const __grid_constant__ CUtensorMap tmap_v,
                        const __nv_bfloat16* __restrict__ q, const DecodeItem* __restrict__ items,
                        const int32_t* __restrict__ tables, __nv_bfloat16* __restrict__ out,
-                       float* __restrict__ part_o, float* __restrict__ part_ml, int subs_per_split,
-                       int n_stages, AttnShape s) {
+                       float* __restrict__ part_o, float* __restrict__ part_ml,
+                       int* __restrict__ counters, int subs_per_split, int n_stages, AttnShape s) {
     using C = DC<HD>;
     constexpr int NT = HD / 8;  // O n-tiles (8 dims each)
     const int kWarpsR = blockDim.x / 32 - 1;  // consumer warps
@@ -293,6 +260,64 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             }
         }
     }
+    if (single) return;
+    // ---------------------------------------------------------------- split merge
+    // Last-arriving split of this (row, kv head) merges all splits in split order (the same
+    // arithmetic as decode_combine_kernel: deterministic), then re-arms the counter.
+    __shared__ int last_s;
+    __threadfence();
+    named_sync(1, kWarpsR * 32);
+    if (threadIdx.x == 0) {
+        int* cnt = counters + blockIdx.x * gridDim.y + kvh;
+        const int prev = atomicAdd(cnt, 1);
+        last_s = prev == static_cast<int>(gridDim.z) - 1;
+        if (last_s) *cnt = 0;
+    }
+    named_sync(1, kWarpsR * 32);
+    if (!last_s) return;
+    __threadfence();
+    // per (head, split) weight exp2(m - M) and the normaliser L, once per head, in smem (the
+    // ring is drained); then one pass over part_o with every split's load in flight
+    const int splits = gridDim.z;
+    float* wsp = reinterpret_cast<float*>(smem);  // [G][splits]
+    float* linv = wsp + 8 * splits;               // [G]
+    float* lsp = linv + 8;  // [G][splits] l
+    for (int i = threadIdx.x; i < G * splits; i += kWarpsR * 32) {  // all (m, l) loads at once
+        const int h = i / splits, sp = i % splits;
+        const size_t sl = ((size_t)blockIdx.x * s.hq + kvh * G + h) * splits + sp;
+        wsp[i] = __ldcg(part_ml + sl * 2);
+        lsp[i] = __ldcg(part_ml + sl * 2 + 1);
+    }
+    named_sync(1, kWarpsR * 32);
+    if (threadIdx.x < G) {
+        float M = -FLT_MAX;
+        for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, wsp[threadIdx.x * splits + sp]);
+        float L = 0.f;
+        for (int sp = 0; sp < splits; ++sp) {
+            const float ls = lsp[threadIdx.x * splits + sp];
+            const float w = ls == 0.f ? 0.f : exp2f(wsp[threadIdx.x * splits + sp] - M);
+            wsp[threadIdx.x * splits + sp] = w;
+            L += ls * w;
+        }
+        linv[threadIdx.x] = L;
+    }
+    named_sync(1, kWarpsR * 32);
+    for (int e = threadIdx.x; e < G * HD; e += kWarpsR * 32) {
+        const int h = e / HD, d = e % HD;
+        const int hh = kvh * G + h;
+        const float* po = part_o + ((size_t)blockIdx.x * s.hq + hh) * splits * HD + d;
+        // every split's load in flight at once (splits <= 16), then the weighted sum in order
+        float pv[16];
+#pragma unroll
+        for (int sp = 0; sp < 16; ++sp) pv[sp] = sp < splits ? __ldcg(po + (size_t)sp * HD) : 0.f;
+        float O = 0.f;
+#pragma unroll
+        for (int sp = 0; sp < 16; ++sp) {
+            const float w = sp < splits ? wsp[h * splits + sp] : 0.f;
+            if (w != 0.f) O += pv[sp] * w;
+        }
+        out[(size_t)it.q_row * s.hq * HD + hh * HD + d] = __float2bfloat16_rn(O / linv[h]);
+    }
 }
 
 // Merge split partials -> normalised bf16 output.  grid = (n_items, hq), block = HD.
@@ -321,7 +346,7 @@ __global__ void decode_combine_kernel(const DecodeItem* __restrict__ items,
 template <int HD>
 cudaError_t launch_hd(const CUtensorMap& tk, const CUtensorMap& tv, const __nv_bfloat16* q,
                       const DecodeItem* items, int n_items, int splits, int sps, const int32_t* tables,
-                      __nv_bfloat16* out, float* po, float* pml, const AttnShape& s, cudaStream_t st) {
+                      __nv_bfloat16* out, float* po, float* pml, int* cnt, const AttnShape& s, cudaStream_t st) {
     using C = DC<HD>;
     static const int warps = std::getenv("ASB_DECODE_WARPS") ? std::atoi(std::getenv("ASB_DECODE_WARPS")) : kWarps;
     static const int stages0 = std::getenv("ASB_DECODE_STAGES") ? std::atoi(std::getenv("ASB_DECODE_STAGES")) : C::kStages;
@@ -330,14 +355,14 @@ cudaError_t launch_hd(const CUtensorMap& tk, const CUtensorMap& tv, const __nv_b
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     dim3 grid(n_items, s.hkv, splits);
     cudaError_t e = launch_k(decode_attn_kernel<HD>, grid, dim3((warps + 1) * 32), smem, st, tk, tv, q, items,
-                             tables, out, po, pml, sps, stages, s);
-    if (e == cudaSuccess && splits > 1)
+                             tables, out, po, pml, cnt, sps, stages, s);
+    if (e == cudaSuccess && splits > 1 && !cnt)
         e = launch_k(decode_combine_kernel<HD>, dim3(n_items, s.hq), dim3(HD), 0, st, items,
                      static_cast<const float*>(po), static_cast<const float*>(pml), splits, out, s.hq);
     return e;
@@ -358,7 +383,7 @@ int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits
 cudaError_t decode_attention(const CUtensorMap& tmap_k32, const CUtensorMap& tmap_v32,
                              const __nv_bfloat16* q, const DecodeItem* items, int n_items,
                              int max_ctx, const int32_t* tables, __nv_bfloat16* out,
-                             float* part_o, float* part_ml, int max_splits, int num_sms,
+                             float* part_o, float* part_ml, int* counters, int max_splits, int num_sms,
                              const AttnShape& s, cudaStream_t stream) {
     if (n_items <= 0) return cudaSuccess;
     if (s.hq / s.hkv > 8) return cudaErrorInvalidValue;
@@ -368,10 +393,10 @@ cudaError_t decode_attention(const CUtensorMap& tmap_k32, const CUtensorMap& tma
     const int splits = (subs + sps - 1) / sps;
     if (s.hd == 128)
         return launch_hd<128>(tmap_k32, tmap_v32, q, items, n_items, splits, sps, tables, out, part_o,
-                              part_ml, s, stream);
+                              part_ml, counters, s, stream);
     if (s.hd == 64)
         return launch_hd<64>(tmap_k32, tmap_v32, q, items, n_items, splits, sps, tables, out, part_o,
-                             part_ml, s, stream);
+                             part_ml, counters, s, stream);
     return cudaErrorInvalidValue;
 }
 

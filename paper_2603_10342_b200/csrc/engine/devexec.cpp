@@ -256,8 +256,8 @@ json DeviceExec::describe() const {
     }
     if (profiling_) {
         static const char* names[ASB_STAT_COUNT] = {"decode_attn", "prefill_attn", "decode_gemm",
-                                                     "prefill_gemm", "forward"};
-        static const char* units[ASB_STAT_COUNT] = {"bytes", "flops", "bytes", "flops", "tokens"};
+                                                     "prefill_gemm", "forward", "decode_step"};
+        static const char* units[ASB_STAT_COUNT] = {"bytes", "flops", "bytes", "flops", "tokens", "bytes"};
         json k = json::object();
         for (int c = 0; c < ASB_STAT_COUNT; ++c) {
             json lanes = json::object();

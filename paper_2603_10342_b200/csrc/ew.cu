@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "attn.h"
+#include "epi.cuh"
 #include "ew.h"
 #include "launch.cuh"
 #include "sm100.cuh"
@@ -59,10 +60,14 @@ __global__ void pack_weights_kernel(const __nv_bfloat16* __restrict__ src, __nv_
 
 // Embedding gather from the tile-packed table: a row is d/64 contiguous 128-byte chunks.
 __global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ emb,
-                             __nv_bfloat16* __restrict__ x, int T, int d) {
+                             __nv_bfloat16* __restrict__ x, int T, int d,
+                             unsigned long long* __restrict__ zero_keys, int n_keys) {
     pdl_trigger();
     pdl_wait();
     const int t = blockIdx.x;
+    // argmax accumulators of this forward's LM head (dgemv path: no final-norm launch)
+    if (zero_keys && t == 0)
+        for (int i = threadIdx.x; i < n_keys; i += blockDim.x) zero_keys[i] = 0ull;
     if (t >= T) return;
     const int64_t R = ids[t];
     const int kb = d / 64;
@@ -90,19 +95,7 @@ __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_
     const uint4* wr = reinterpret_cast<const uint4*>(w);
     uint4* yr = reinterpret_cast<uint4*>(y + static_cast<size_t>(row) * d);
     const int nv = d / 8;
-    float ss = 0.f;
-    for (int i = lane; i < nv; i += 32) {
-        const uint4 v = xr[i];
-        const uint32_t a[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float lo = bf16_lo(a[e]), hi = bf16_hi(a[e]);
-            ss += lo * lo + hi * hi;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, static_cast<float>(d)), eps)));
+    const float inv = rms_inv_warp(x + static_cast<size_t>(src_row) * d, d, eps, lane);
     for (int i = lane; i < nv; i += 32) {
         const uint4 v = xr[i], g = wr[i];
         const uint32_t a[4] = {v.x, v.y, v.z, v.w};
@@ -212,9 +205,9 @@ cudaError_t pack_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, int64_t r
 }
 
 cudaError_t embed(const int32_t* ids, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int d,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, unsigned long long* zero_keys, int n_keys) {
     if (T <= 0) return cudaSuccess;
-    return launch_k(embed_kernel, dim3(T), dim3(128), 0, stream, ids, emb, x, T, d);
+    return launch_k(embed_kernel, dim3(T), dim3(128), 0, stream, ids, emb, x, T, d, zero_keys, n_keys);
 }
 
 cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows_idx, const __nv_bfloat16* w,

@@ -33,6 +33,7 @@
 #include <tuple>
 
 #include "attn.h"
+#include "epi.cuh"
 #include "gemm.h"
 #include "sm100.cuh"
 
@@ -55,8 +56,6 @@ struct GemmCfg {
     // cluster split-K parks a [BN tokens][128 rows] fp32 partial in the (drained) ring
     static_assert(BN * BM * 4 <= kStages * kStageBytes, "partial does not fit the ring");
 };
-
-__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // Apply the epilogue to one output value (all modes except SiLU).
 struct Epi {
@@ -126,20 +125,7 @@ struct Epi {
     }
 };
 
-// ---- fused QKV epilogue helpers (EPI_QKV) ----------------------------------------------
-__device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
-
-__device__ __forceinline__ size_t pool_off(const RopeEpi& R, int slot, int kv_head) {
-    const int blk = slot / kBlockTokens, off = slot % kBlockTokens;
-    return ((((size_t)R.layer * R.num_blocks + blk) * R.hkv + kv_head) * kBlockTokens + off) * R.hd;
-}
-
-// rotate_half pair at one cos/sin column (same op order as rope_append_kernel)
-__device__ __forceinline__ void rope2(float x1, float x2, float c, float s, float& y1, float& y2) {
-    y1 = __fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, s));
-    y2 = __fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, s));
-}
-
+// ---- fused QKV epilogue helpers (EPI_QKV); bf16r / pool_off / rope2 live in epi.cuh
 __device__ __forceinline__ void store32_bf16(__nv_bfloat16* dst, const float (&v)[32]) {
     uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll

@@ -47,6 +47,33 @@ struct GemmParams {
     unsigned long long* dbg_times;  // optional per-CTA timeline [grid][8] (globaltimer ns)
 };
 
+// Small-batch decode linear (dgemv.cu): T <= dgemv_max_tokens() rows of X against a
+// tile-packed W, legacy warp MMAs fed straight from HBM, optional fused RMSNorm of X.
+// Epilogue fields (epi, out, out_f32, ldo, bias, resid, ldr, rope, amax) mean what they mean
+// in GemmParams; EPI_F32 + amax keeps a per-token greedy-argmax key (zeroed by the caller).
+struct DgemvParams {
+    const __nv_bfloat16* w;  // packed [rows_pad/128][K/64][128][64]
+    int rows_pad;
+    const __nv_bfloat16* x;  // [*][ldx]; row of token t = x_rows ? x_rows[t] : t
+    const int32_t* x_rows;
+    int ldx;
+    int T, n_out, K;
+    const __nv_bfloat16* norm_w;  // non-null: X := bf16(X * rms_inv(X) * norm_w) (over K)
+    float eps;
+    int epi;
+    __nv_bfloat16* out;
+    float* out_f32;
+    int ldo;
+    const __nv_bfloat16* bias;
+    const __nv_bfloat16* resid;
+    int ldr;
+    RopeEpi rope;
+    unsigned long long* amax;
+    int rw;  // internal: row-warps per CTA
+};
+int dgemv_max_tokens();
+cudaError_t dgemv_launch(DgemvParams p, int num_sms, cudaStream_t stream);
+
 int gemm_pick_bn(int n);
 int gemm_smem_bytes(int bn);
 // Cluster split-K factor for a swap-path GEMM of `tiles` weight tiles: the largest S <= 8

@@ -18,10 +18,12 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <cstdio>
 #include <vector>
 
 #include "../../include/agentserve_b200.h"
 #include "attn.h"
+#include "decode_step.h"
 #include "ew.h"
 #include "gemm.h"
 #include "launch.cuh"
@@ -197,6 +199,7 @@ struct asb_model {
     };
     std::vector<Layer> layers;
     float *cos_t = nullptr, *sin_t = nullptr;
+    MkLayer* mk_layers = nullptr;  // device copy of the per-layer pointers (decode-step kernel)
 
     ~asb_model() {
         cudaSetDevice(device);
@@ -268,6 +271,20 @@ struct asb_lane {
     int max_T = 0, max_segs = 0, max_tbl = 0, max_pitems = 0, max_splits = 16;
     __nv_bfloat16 *x, *h, *qkv, *q, *attn, *act, *hl;
     float *logits, *part_o, *part_ml, *ppart_o, *ppart_ml;
+    int* dcnt = nullptr;  // decode-attention split arrival counters [rows][hkv] (self-resetting)
+    // split merge inside the decode-attention kernel (last-arriving split) instead of a
+    // combine launch; ASB_ATTN_COMBINE=1 selects the separate combine kernel
+    bool attn_fused_merge = std::getenv("ASB_ATTN_COMBINE") == nullptr;
+    // persistent decode-step kernel (decode_step.cu): grid barrier, split-tile and attention
+    // workspaces; mega = 0 after a failed cooperative launch (kernel-per-op path from then on)
+    unsigned* mk_bar = nullptr;
+    int* mk_tile_cnt = nullptr;
+    float *mk_ws = nullptr, *mk_apo = nullptr, *mk_apml = nullptr;
+    int* mk_acnt = nullptr;
+    int mk_max_spl = 16;
+    unsigned long long* mk_dbg = nullptr;  // ASB_MK_TIMELINE=1: per-CTA phase start stamps
+    bool mega = std::getenv("ASB_MEGA") != nullptr && std::atoi(std::getenv("ASB_MEGA")) != 0;  // opt-in
+    CUtensorMap map_x[5];
     bool pdl = std::getenv("ASB_NO_PDL") == nullptr;  // programmatic dependent launch
     unsigned long long* dbg_times = nullptr;  // ASB_GEMM_TIMELINE: per-CTA stamps of the last GEMM
     size_t ppart_rows = 0;
@@ -361,11 +378,67 @@ void act_maps(CUtensorMap* maps, const void* base, int rows, int cols) {
 
 int swap_map_index(int bn) { return bn == 32 ? 1 : bn == 64 ? 2 : bn == 128 ? 3 : 4; }
 
-// Y[T][n_out] = X[T][k] . W^T with the path chosen by T.
-void linear(asb_lane* L, const CUtensorMap* xmaps, const Weight& w, int T, int epi,
+// The X operand of a linear layer: TMA maps for the tcgen05 paths, the raw rows for the
+// small-batch dgemv path, which can also apply the layer's RMSNorm on the fly (norm_w) and
+// gather its rows (rows, the LM-head logit rows).
+struct XIn {
+    const CUtensorMap* maps;
+    const __nv_bfloat16* ptr;
+    int ld;
+    const __nv_bfloat16* norm_w = nullptr;
+    const int32_t* rows = nullptr;
+    float eps = 0.f;
+};
+
+// Small-batch decode path for this linear?  dgemv wins where the launch is latency-bound
+// (few weight bytes); above ~24 MB of weights the tcgen05 swap-AB kernel already streams at
+// ~6 TB/s (profiles/r1_gemm_bench_dgemv.json).  ASB_NO_DGEMV=1: tcgen05 everywhere.
+bool use_dgemv(int T, const Weight& w, int num_sms) {
+    static const bool off = std::getenv("ASB_NO_DGEMV") && std::atoi(std::getenv("ASB_NO_DGEMV")) != 0;
+    const double bytes = 2.0 * double(w.rows) * w.cols;
+    // measured crossover (profiles/r1_gemm_bench_partitions.json): dgemv wins while each SM
+    // of the partition streams <= ~160 KB of the weight; beyond that the TMA-fed tcgen05
+    // kernel keeps more bytes in flight per SM
+    return !off && T <= (bytes / num_sms <= 160e3 ? 16 : 0);
+}
+
+// Y[T][n_out] = X[T][k] . W^T with the path chosen by T (path 2 = dgemv, 1 = tcgen05
+// swap-AB, 0 = tcgen05 normal).
+void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
             __nv_bfloat16* out, int ldo, const __nv_bfloat16* bias, const __nv_bfloat16* resid,
             float* out_f32, int force_path = -1, int force_splits = 0,
             unsigned long long* amax = nullptr, const RopeEpi* rope = nullptr) {
+    const CUtensorMap* xmaps = xin.maps;
+    if (force_path == 2 || (force_path < 0 && use_dgemv(T, w, L->n_sms()))) {
+        DgemvParams d{};
+        d.w = w.ptr;
+        d.rows_pad = w.rows_pad;
+        d.x = xin.ptr;
+        d.x_rows = xin.rows;
+        d.ldx = xin.ld;
+        d.T = T;
+        d.n_out = w.rows;
+        d.K = w.cols;
+        d.norm_w = xin.norm_w;
+        d.eps = xin.eps;
+        d.epi = epi;
+        d.out = out;
+        d.out_f32 = out_f32;
+        d.ldo = ldo;
+        d.bias = bias;
+        d.resid = resid;
+        d.ldr = ldo;
+        if (rope) d.rope = *rope;
+        d.amax = amax;
+        L->n_launch += 1;
+        const double units = 2.0 * (double(w.rows) * w.cols + double(T) * w.cols) +
+                             double(T) * w.rows * (epi == EPI_F32 ? 4.0 : 2.0);
+        cudaError_t e = cudaSuccess;
+        L->timed(ASB_STAT_DECODE_GEMM, units, [&] { e = dgemv_launch(d, L->n_sms(), L->stream); });
+        cuda_check(e, "dgemv launch");
+        return;
+    }
+    if (xin.norm_w || xin.rows) fail(ASB_ERR_INVALID_ARGUMENT, "fused norm / row gather needs the dgemv path");
     GemmParams p{};
     p.amax = amax;
     if (rope) p.rope = *rope;
@@ -535,6 +608,15 @@ asb_status asb_model_create(const char* model, uint64_t seed, int device, int ma
         m->sin_t = static_cast<float*>(dmalloc(sn.size() * 4, m->allocs));
         cuda_check(cudaMemcpy(m->cos_t, c.data(), c.size() * 4, cudaMemcpyHostToDevice), "copy rope");
         cuda_check(cudaMemcpy(m->sin_t, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice), "copy rope");
+        {
+            std::vector<MkLayer> mk;
+            for (const auto& ly : m->layers)
+                mk.push_back(MkLayer{ly.qkv.ptr, ly.o.ptr, ly.gate_up.ptr, ly.down.ptr, ly.attn_norm, ly.mlp_norm,
+                                     ly.qkv_bias});
+            m->mk_layers = static_cast<MkLayer*>(dmalloc(mk.size() * sizeof(MkLayer), m->allocs));
+            cuda_check(cudaMemcpy(m->mk_layers, mk.data(), mk.size() * sizeof(MkLayer), cudaMemcpyHostToDevice),
+                       "copy layer table");
+        }
         cuda_check(cudaDeviceSynchronize(), "weight init");
         *out = m.release();
     });
@@ -741,6 +823,26 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
             dmalloc(size_t(dec_rows) * s.hq * L->max_splits * s.hd * 4, L->allocs));
         L->part_ml = static_cast<float*>(
             dmalloc(size_t(dec_rows) * s.hq * L->max_splits * 2 * 4, L->allocs));
+        L->dcnt = static_cast<int*>(dmalloc(size_t(dec_rows) * s.hkv * 4, L->allocs));
+        cuda_check(cudaMemset(L->dcnt, 0, size_t(dec_rows) * s.hkv * 4), "counters");
+        {
+            const int rows = kMkMaxRows, G = s.hq / s.hkv;
+            const int max_n = std::max({s.vocab, 2 * s.ffn, (s.hq + 2 * s.hkv) * s.hd, s.d});
+            L->mk_bar = static_cast<unsigned*>(dmalloc(256, L->allocs));  // [0] arrivals, [32] generation
+            L->mk_tile_cnt = static_cast<int*>(dmalloc(size_t(max_n / 128 + 2) * 4, L->allocs));
+            L->mk_ws = static_cast<float*>(dmalloc(size_t(m->num_sms) * 2 * 128 * 32 * 4, L->allocs));
+            L->mk_apo = static_cast<float*>(dmalloc(size_t(rows) * s.hkv * L->mk_max_spl * G * s.hd * 4, L->allocs));
+            L->mk_apml = static_cast<float*>(dmalloc(size_t(rows) * s.hkv * L->mk_max_spl * G * 2 * 4, L->allocs));
+            L->mk_acnt = static_cast<int*>(dmalloc(size_t(rows) * s.hkv * 4, L->allocs));
+            cuda_check(cudaMemset(L->mk_bar, 0, 256), "mk");
+            cuda_check(cudaMemset(L->mk_tile_cnt, 0, size_t(max_n / 128 + 2) * 4), "mk");
+            cuda_check(cudaMemset(L->mk_acnt, 0, size_t(rows) * s.hkv * 4), "mk");
+            if (std::getenv("ASB_MK_TIMELINE")) {
+                L->mk_dbg = static_cast<unsigned long long*>(
+                    dmalloc(size_t(m->num_sms) * kMkDbgSlots * 8, L->allocs));
+                cuda_check(cudaMemset(L->mk_dbg, 0, size_t(m->num_sms) * kMkDbgSlots * 8), "mk");
+            }
+        }
         // split-KV partials for small prefill grids (resume chunks): <= 4096 rows of 128 queries
         L->ppart_rows = size_t(4096) * 256 / 16;
         L->ppart_o = static_cast<float*>(dmalloc(L->ppart_rows * s.hd * 4, L->allocs));
@@ -752,6 +854,7 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->d_out = static_cast<unsigned long long*>(dmalloc(size_t(L->max_segs) * 8, L->allocs));
         cuda_check(cudaMallocHost(&L->h_out, size_t(L->max_segs) * 8), "cudaMallocHost");
         act_maps(L->map_h, L->h, T, s.d);
+        act_maps(L->map_x, L->x, T, s.d);
         act_maps(L->map_attn, L->attn, T, qd);
         act_maps(L->map_act, L->act, T, s.ffn);
         act_maps(L->map_hl, L->hl, L->max_segs, s.d);
@@ -873,10 +976,6 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         cuda_check(cudaEventRecord(L->ev0, st), "event");
         cuda_check(cudaMemcpyAsync(L->d_meta, hm, used * 4, cudaMemcpyHostToDevice, st), "meta H2D");
         L->h2d += int64_t(used) * 4;
-        // kernels per forward: embed + per layer (2 norms, rope, 4 GEMMs (+finalize), attention
-        // (decode: 2, prefill: 1)) + final norm / LM head / argmax
-        L->n_launch += 1 + int64_t(s.layers) * (3 + (ditems.empty() ? 0 : 2) + (pitems.empty() ? 0 : 1)) +
-                       (n_logit > 0 ? 2 : 0);
         const int32_t* d_tok = L->d_meta;
         const int32_t* d_pos = d_tok + T;
         const int32_t* d_slot = d_pos + T;
@@ -908,64 +1007,163 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         cudaEvent_t fwd_a = L->prof ? L->take_event() : nullptr;
         if (fwd_a) cuda_check(cudaEventRecord(fwd_a, st), "event");
         PdlScope pdl_scope(L->pdl && !L->prof);
-        cuda_check(embed(d_tok, m->embed.ptr, L->x, T, s.d, st), "embed");
-        // the fused QKV epilogue needs q/k/v regions aligned to the 128-row weight tiles
-        // ASB_DEBUG_SKIP=attn,norm,...: timing ablation only (outputs are garbage)
-        static const std::string skip_list = std::getenv("ASB_DEBUG_SKIP") ? std::getenv("ASB_DEBUG_SKIP") : "";
-        auto skip = [&](const char* what) {
-            return !skip_list.empty() && ("," + skip_list + ",").find("," + std::string(what) + ",") != std::string::npos;
-        };
-        const bool fuse_qkv = (qd % 128 == 0) && (kvd % 128 == 0) && (s.hd == 64 || s.hd == 128) &&
-                              std::getenv("ASB_NO_QKV_FUSION") == nullptr;
-        for (int l = 0; l < s.layers; ++l) {
-            const auto& ly = m->layers[l];
-            as.layer = l;
-            if (!skip("norm")) cuda_check(rmsnorm(L->x, nullptr, ly.attn_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
-            if (skip("qkv")) {
-            } else if (fuse_qkv) {
-                // QKV GEMM with bias, RoPE and the paged K/V append fused into its epilogue
-                RopeEpi re{d_pos, d_slot, m->cos_t, m->sin_t, L->q, kv->k_pool, kv->v_pool,
-                           s.hq, s.hkv, s.hd, l, kv->nb};
-                linear(L, L->map_h, ly.qkv, T, EPI_QKV, nullptr, qd + 2 * kvd, ly.qkv_bias, nullptr, nullptr,
-                       -1, 0, nullptr, &re);
+        // Decode-only steps of <= 16 rows: one persistent launch for the whole forward
+        // (decode_step.cu).  A failed cooperative launch (partition too small for the grid)
+        // switches the lane to the kernel-per-op path below for good.
+        bool mega_done = false;
+        if (L->mega && pitems.empty() && int(ditems.size()) == n_segs && T <= kMkMaxRows && n_logit == T &&
+            s.hq / s.hkv <= 8 && (s.hd == 64 || s.hd == 128) && s.d % 64 == 0 && s.d <= 1024 && s.ffn % 64 == 0 &&
+            (s.hq * s.hd) % 64 == 0 && std::getenv("ASB_DEBUG_SKIP") == nullptr) {
+            MkMaps mm{L->map_x[1], L->map_attn[1], L->map_act[1], kv->tk32, kv->tv32};
+            MkParams mp{};
+            mp.layers = m->mk_layers;
+            mp.L = s.layers;
+            mp.d = s.d;
+            mp.hq = s.hq;
+            mp.hkv = s.hkv;
+            mp.hd = s.hd;
+            mp.ffn = s.ffn;
+            mp.vocab = s.vocab;
+            mp.eps = s.eps;
+            mp.scale_log2 = as.scale_log2;
+            mp.T = T;
+            mp.G = std::min(L->n_sms(), m->num_sms);
+            const int n_items = T * s.hkv;
+            mp.attn_spl = std::max(1, std::min({mp.G / n_items, L->mk_max_spl, (max_ctx + 31) / 32}));
+            mp.tok = d_tok;
+            mp.pos = d_pos;
+            mp.slot = d_slot;
+            mp.items = d_ditems;
+            mp.tables = d_tbl;
+            mp.embed = m->embed.ptr;
+            mp.lm_head = m->lm_head.ptr;
+            mp.final_norm = m->final_norm;
+            mp.x = L->x;
+            mp.q = L->q;
+            mp.attn = L->attn;
+            mp.act = L->act;
+            mp.logits = L->logits;
+            mp.keys = L->d_out;
+            mp.k_pool = kv->k_pool;
+            mp.v_pool = kv->v_pool;
+            mp.num_blocks = kv->nb;
+            mp.cos_t = m->cos_t;
+            mp.sin_t = m->sin_t;
+            mp.bar = L->mk_bar;
+            mp.tile_cnt = L->mk_tile_cnt;
+            mp.ws = L->mk_ws;
+            mp.apart_o = L->mk_apo;
+            mp.apart_ml = L->mk_apml;
+            mp.acnt = L->mk_acnt;
+            mp.dbg = L->mk_dbg;
+            // algorithmic bytes: every weight once + every context token's K and V once
+            double wbytes = 2.0 * double(m->lm_head.rows) * m->lm_head.cols;
+            for (const auto& ly : m->layers)
+                wbytes += 2.0 * (double(ly.qkv.rows) * ly.qkv.cols + double(ly.o.rows) * ly.o.cols +
+                                 double(ly.gate_up.rows) * ly.gate_up.cols + double(ly.down.rows) * ly.down.cols);
+            cudaError_t e = cudaSuccess;
+            L->timed(ASB_STAT_DECODE_STEP, wbytes + dattn_bytes * s.layers,
+                     [&] { e = decode_step_launch(mm, mp, st); });
+            if (e == cudaSuccess) {
+                mega_done = true;
+                L->n_launch += 1;
+                cuda_check(cudaMemcpyAsync(L->h_out, L->d_out, n_logit * 8, cudaMemcpyDeviceToHost, st), "ids D2H");
+                L->d2h += int64_t(n_logit) * 8;
             } else {
-                linear(L, L->map_h, ly.qkv, T, EPI_BF16, L->qkv, qd + 2 * kvd, ly.qkv_bias, nullptr, nullptr);
-                cuda_check(rope_append(L->qkv, d_pos, d_slot, m->cos_t, m->sin_t, L->q, kv->k_pool,
-                                       kv->v_pool, T, s.hq, s.hkv, s.hd, l, kv->nb, st),
-                           "rope_append");
+                cudaGetLastError();
+                L->mega = false;
+                std::fprintf(stderr, "[agentserve_b200] decode-step kernel unavailable (%s, grid %d): "
+                             "kernel-per-op decode from now on\n", cudaGetErrorString(e), mp.G);
             }
-            if (!ditems.empty() && !skip("attn"))
-                L->timed(ASB_STAT_DECODE_ATTN, dattn_bytes, [&] {
-                    cuda_check(decode_attention(kv->tk32, kv->tv32, L->q, d_ditems, int(ditems.size()),
-                                                max_ctx, d_tbl, L->attn, L->part_o, L->part_ml,
-                                                L->max_splits, L->n_sms(), as, st),
-                               "decode attention");
-                });
-            if (!pitems.empty())
-                L->timed(ASB_STAT_PREFILL_ATTN, pattn_flops, [&] {
-                    cuda_check(prefill_attention(L->map_q, kv->tk, kv->tv, d_pitems, int(pitems.size()),
-                                                 max_pblocks, psplits, d_tbl, L->attn, L->ppart_o,
-                                                 L->ppart_ml, as, st),
-                               "prefill attention");
-                });
-            if (!skip("o")) linear(L, L->map_attn, ly.o, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
-            if (!skip("norm")) cuda_check(rmsnorm(L->x, nullptr, ly.mlp_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
-            if (!skip("gate_up")) linear(L, L->map_h, ly.gate_up, T, EPI_SILU, L->act, s.ffn, nullptr, nullptr, nullptr);
-            if (!skip("down")) linear(L, L->map_act, ly.down, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
         }
-        if (n_logit > 0) {
-            // greedy sample fused into the LM head epilogue (swap path, <= 256 rows): the norm
-            // zeroes the per-row argmax keys, the GEMM atomicMax-es into them
-            const bool fused_argmax = n_logit <= 256;
-            cuda_check(rmsnorm(L->x, d_lrows, m->final_norm, L->hl, n_logit, s.d, s.eps, st,
-                               fused_argmax ? L->d_out : nullptr), "final norm");
-            linear(L, L->map_hl, m->lm_head, n_logit, EPI_F32, nullptr, s.vocab, nullptr, nullptr,
-                   L->logits, -1, 0, fused_argmax ? L->d_out : nullptr);
-            if (!fused_argmax)
-                cuda_check(argmax_rows(L->logits, n_logit, s.vocab, s.vocab, L->d_out, st), "argmax");
-            cuda_check(cudaMemcpyAsync(L->h_out, L->d_out, n_logit * 8, cudaMemcpyDeviceToHost, st),
-                       "ids D2H");
-            L->d2h += int64_t(n_logit) * 8;
+        if (!mega_done) {
+            cuda_check(embed(d_tok, m->embed.ptr, L->x, T, s.d, st,
+                             (n_logit > 0 && use_dgemv(n_logit, m->lm_head, L->n_sms())) ? L->d_out : nullptr, n_logit),
+                       "embed");
+            // the fused QKV epilogue needs q/k/v regions aligned to the 128-row weight tiles
+            // ASB_DEBUG_SKIP=attn,norm,...: timing ablation only (outputs are garbage)
+            static const std::string skip_list = std::getenv("ASB_DEBUG_SKIP") ? std::getenv("ASB_DEBUG_SKIP") : "";
+            auto skip = [&](const char* what) {
+                return !skip_list.empty() && ("," + skip_list + ",").find("," + std::string(what) + ",") != std::string::npos;
+            };
+            const bool fuse_qkv = (qd % 128 == 0) && (kvd % 128 == 0) && (s.hd == 64 || s.hd == 128) &&
+                                  std::getenv("ASB_NO_QKV_FUSION") == nullptr;
+            // Small batches (decode steps) take the dgemv path where it wins; its QKV / gate-up /
+            // LM-head launches apply the preceding RMSNorm themselves (no norm launch).
+            const bool dg_qkv = use_dgemv(T, m->layers[0].qkv, L->n_sms()),
+                       dg_gu = use_dgemv(T, m->layers[0].gate_up, L->n_sms());
+            // non-GEMM kernels of this forward (linear() counts its own launches): embed; per layer
+            // the unfused norms, the unfused RoPE/append, decode attention (split merge fused) and
+            // prefill attention (+ its split combine); final norm and argmax when not fused
+            L->n_launch += 1 + int64_t(s.layers) * ((dg_qkv ? 0 : 1) + (dg_gu ? 0 : 1) + (fuse_qkv ? 0 : 1) +
+                                                    (ditems.empty() ? 0 : 1) +
+                                                    (pitems.empty() ? 0 : (psplits > 1 ? 2 : 1)));
+            if (n_logit > 0 && !use_dgemv(n_logit, m->lm_head, L->n_sms())) L->n_launch += n_logit <= 256 ? 1 : 2;
+            const XIn x_attn{L->map_attn, L->attn, qd};
+            const XIn x_act{L->map_act, L->act, s.ffn};
+            for (int l = 0; l < s.layers; ++l) {
+                const auto& ly = m->layers[l];
+                as.layer = l;
+                const XIn xa = dg_qkv ? XIn{nullptr, L->x, s.d, ly.attn_norm, nullptr, s.eps}
+                                      : XIn{L->map_h, L->h, s.d};
+                const XIn xm = dg_gu ? XIn{nullptr, L->x, s.d, ly.mlp_norm, nullptr, s.eps}
+                                     : XIn{L->map_h, L->h, s.d};
+                if (!dg_qkv && !skip("norm"))
+                    cuda_check(rmsnorm(L->x, nullptr, ly.attn_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
+                if (skip("qkv")) {
+                } else if (fuse_qkv) {
+                    // QKV GEMM with bias, RoPE and the paged K/V append fused into its epilogue
+                    RopeEpi re{d_pos, d_slot, m->cos_t, m->sin_t, L->q, kv->k_pool, kv->v_pool,
+                               s.hq, s.hkv, s.hd, l, kv->nb};
+                    linear(L, xa, ly.qkv, T, EPI_QKV, nullptr, qd + 2 * kvd, ly.qkv_bias, nullptr, nullptr,
+                           -1, 0, nullptr, &re);
+                } else {
+                    linear(L, xa, ly.qkv, T, EPI_BF16, L->qkv, qd + 2 * kvd, ly.qkv_bias, nullptr, nullptr);
+                    cuda_check(rope_append(L->qkv, d_pos, d_slot, m->cos_t, m->sin_t, L->q, kv->k_pool,
+                                           kv->v_pool, T, s.hq, s.hkv, s.hd, l, kv->nb, st),
+                               "rope_append");
+                }
+                if (!ditems.empty() && !skip("attn"))
+                    L->timed(ASB_STAT_DECODE_ATTN, dattn_bytes, [&] {
+                        cuda_check(decode_attention(kv->tk32, kv->tv32, L->q, d_ditems, int(ditems.size()),
+                                                    max_ctx, d_tbl, L->attn, L->part_o, L->part_ml,
+                                                    L->dcnt, L->max_splits, L->n_sms(), as, st),
+                                   "decode attention");
+                    });
+                if (!pitems.empty())
+                    L->timed(ASB_STAT_PREFILL_ATTN, pattn_flops, [&] {
+                        cuda_check(prefill_attention(L->map_q, kv->tk, kv->tv, d_pitems, int(pitems.size()),
+                                                     max_pblocks, psplits, d_tbl, L->attn, L->ppart_o,
+                                                     L->ppart_ml, as, st),
+                                   "prefill attention");
+                    });
+                if (!skip("o")) linear(L, x_attn, ly.o, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
+                if (!dg_gu && !skip("norm"))
+                    cuda_check(rmsnorm(L->x, nullptr, ly.mlp_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
+                if (!skip("gate_up")) linear(L, xm, ly.gate_up, T, EPI_SILU, L->act, s.ffn, nullptr, nullptr, nullptr);
+                if (!skip("down")) linear(L, x_act, ly.down, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
+            }
+            if (n_logit > 0) {
+                // greedy sample fused into the LM head epilogue (<= 256 rows): the argmax keys are
+                // zeroed by the final norm (or, on the dgemv path, by the embedding kernel, and the
+                // LM head normalises and gathers its rows itself); the GEMM atomicMax-es into them
+                const bool fused_argmax = n_logit <= 256;
+                if (use_dgemv(n_logit, m->lm_head, L->n_sms())) {
+                    XIn xl{nullptr, L->x, s.d, m->final_norm, d_lrows, s.eps};
+                    linear(L, xl, m->lm_head, n_logit, EPI_F32, nullptr, s.vocab, nullptr, nullptr, L->logits, -1, 0,
+                           L->d_out);
+                } else {
+                    cuda_check(rmsnorm(L->x, d_lrows, m->final_norm, L->hl, n_logit, s.d, s.eps, st,
+                                       fused_argmax ? L->d_out : nullptr), "final norm");
+                    linear(L, XIn{L->map_hl, L->hl, s.d}, m->lm_head, n_logit, EPI_F32, nullptr, s.vocab, nullptr,
+                           nullptr, L->logits, -1, 0, fused_argmax ? L->d_out : nullptr);
+                    if (!fused_argmax)
+                        cuda_check(argmax_rows(L->logits, n_logit, s.vocab, s.vocab, L->d_out, st), "argmax");
+                }
+                cuda_check(cudaMemcpyAsync(L->h_out, L->d_out, n_logit * 8, cudaMemcpyDeviceToHost, st),
+                           "ids D2H");
+                L->d2h += int64_t(n_logit) * 8;
+            }
         }
         if (fwd_a) {
             cudaEvent_t fwd_b = L->take_event();
@@ -990,6 +1188,17 @@ asb_status asb_debug_gemm_timeline(asb_lane* L, unsigned long long* out, int n) 
     return guarded([&] {
         cuda_check(cudaStreamSynchronize(L->stream), "timeline");
         cuda_check(cudaMemcpy(out, L->dbg_times, size_t(std::min(n, 148 * 8)) * 8, cudaMemcpyDeviceToHost), "timeline");
+    });
+}
+
+asb_status asb_debug_mk_timeline(asb_lane* L, unsigned long long* out, int n) {
+    if (!L || !out) return ASB_ERR_INVALID_ARGUMENT;
+    return guarded([&] {
+        if (!L->mk_dbg) fail(ASB_ERR_NO_DATA, "lane created without ASB_MK_TIMELINE=1");
+        cuda_check(cudaStreamSynchronize(L->stream), "sync");
+        const size_t total = size_t(L->m->num_sms) * kMkDbgSlots;
+        cuda_check(cudaMemcpy(out, L->mk_dbg, std::min<size_t>(total, size_t(n)) * 8, cudaMemcpyDeviceToHost),
+                   "timeline");
     });
 }
 
@@ -1073,6 +1282,72 @@ asb_status asb_decode_launch(asb_lane* lane, asb_kv* kv, const uint32_t* session
     return asb_forward(lane, kv, segs.data(), int(segs.size()), toks.data());
 }
 
+// Back-to-back timing of one linear layer: weights packed once into enough copies to exceed
+// L2 (cycled, so each launch streams from HBM as in a real step); `reps` launches with PDL,
+// bracketed by CUDA events: average microseconds per launch.  num_sms = 0: all.
+asb_status asb_debug_gemm_bench(const void* x, const void* w, void* out, int tokens, int n_out, int k,
+                                int epi, int force_path, int reps, int num_sms, void* stream,
+                                float* us_per_launch) {
+    if (!us_per_launch || reps < 1) {
+        g_err = "invalid argument";
+        return ASB_ERR_INVALID_ARGUMENT;
+    }
+    return guarded([&] {
+        // enough packed copies to exceed the 126 MB L2, cycled, so every launch streams from HBM
+        const size_t wbytes = size_t((n_out + 127) / 128 * 128) * k * 2;
+        const int copies = int(std::min<size_t>(256, (size_t(320) << 20) / wbytes + 1));
+        std::vector<Weight> Ws(copies);
+        for (auto& W : Ws) {
+            W.rows = n_out;
+            W.rows_pad = (n_out + 127) / 128 * 128;
+            W.cols = k;
+            cuda_check(cudaMalloc(&W.ptr, wbytes), "packed w");
+            cuda_check(cudaMemset(W.ptr, 0, wbytes), "packed w");
+            cuda_check(pack_weights(static_cast<const __nv_bfloat16*>(w), W.ptr, n_out, k, nullptr), "pack");
+            weight_maps(W);
+        }
+        CUtensorMap xm[5];
+        act_maps(xm, x, tokens, k);
+        asb_model fake;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, dev), "props");
+        fake.device = dev;
+        fake.num_sms = num_sms > 0 ? num_sms : prop.multiProcessorCount;
+        asb_lane tmp;
+        tmp.m = &fake;
+        if (stream) tmp.stream = static_cast<cudaStream_t>(stream);
+        else cuda_check(cudaStreamCreateWithFlags(&tmp.stream, cudaStreamNonBlocking), "stream");
+        const int ldo = epi == EPI_SILU ? n_out / 2 : n_out;
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        auto run = [&](int n) {
+            PdlScope pdl(true);
+            for (int i = 0; i < n; ++i)
+                linear(&tmp, XIn{xm, static_cast<const __nv_bfloat16*>(x), k}, Ws[i % copies], tokens, epi,
+                       static_cast<__nv_bfloat16*>(out), ldo, nullptr,
+                       epi == EPI_RESID ? static_cast<const __nv_bfloat16*>(out) : nullptr,
+                       epi == EPI_F32 ? static_cast<float*>(out) : nullptr, force_path, 0);
+        };
+        run(3);
+        cuda_check(cudaEventRecord(e0, tmp.stream), "event");
+        run(reps);
+        cuda_check(cudaEventRecord(e1, tmp.stream), "event");
+        cuda_check(cudaEventSynchronize(e1), "bench sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        *us_per_launch = 1000.f * ms / reps;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (!stream) cudaStreamDestroy(tmp.stream);
+        tmp.stream = nullptr;
+        for (auto& W : Ws) cudaFree(W.ptr);
+        tmp.m = &fake;
+    });
+}
+
 asb_status asb_debug_gemm(const void* x, const void* w, const void* bias, const void* resid,
                           void* out, int tokens, int n_out, int k, int epi, int force_path,
                           int splits, void* stream) {
@@ -1103,7 +1378,8 @@ asb_status asb_debug_gemm(const void* x, const void* w, const void* bias, const 
             cuda_check(cudaMalloc(&tmp.dbg_times, 148 * 8 * 8), "timeline");
             cuda_check(cudaMemset(tmp.dbg_times, 0, 148 * 8 * 8), "timeline");
         }
-        linear(&tmp, xm, W, tokens, epi, static_cast<__nv_bfloat16*>(out), ldo,
+        linear(&tmp, XIn{xm, static_cast<const __nv_bfloat16*>(x), k}, W, tokens, epi,
+               static_cast<__nv_bfloat16*>(out), ldo,
                static_cast<const __nv_bfloat16*>(bias), static_cast<const __nv_bfloat16*>(resid),
                epi == EPI_F32 ? static_cast<float*>(out) : nullptr, force_path, splits);
         cuda_check(cudaStreamSynchronize(tmp.stream), "debug gemm");

@@ -135,7 +135,7 @@ class Lane:
         """SM count the lane sizes its grids for (the partition its stream runs on)."""
         check(lib().asb_lane_set_sms(self.h, sms))
 
-    CATS = ("decode_attn", "prefill_attn", "decode_gemm", "prefill_gemm", "forward")
+    CATS = ("decode_attn", "prefill_attn", "decode_gemm", "prefill_gemm", "forward", "decode_step")
 
     def profile(self, on: bool = True) -> None:
         check(lib().asb_lane_profile(self.h, 1 if on else 0))

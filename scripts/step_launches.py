@@ -12,13 +12,15 @@ import numpy as np
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-from paper_2603_10342_b200.device import KvPool, Lane, Model  # noqa: E402
+from paper_2603_10342_b200.device import KvPool, Lane, Model, Slots  # noqa: E402
 
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 name = args[0] if args else "qwen2.5-0.5b"
 B = int(args[1]) if len(args) > 1 else 8
 ctx = int(args[2]) if len(args) > 2 else 2048
 ncu = "--ncu" in sys.argv
+level = int([a for a in sys.argv if a.startswith("--level=")][0].split("=")[1]) if any(
+    a.startswith("--level=") for a in sys.argv) else 0
 m = Model(name, seed=13, max_context=ctx + 256)
 kv = KvPool(m, num_blocks=B * ((ctx + 63) // 64 + 2) + 8)
 lane = Lane(m, max_tokens=2048, max_segments=B + 4)
@@ -30,6 +32,11 @@ for s in range(B):
         lane.forward(kv, [(s, n, 0)], rng.integers(0, m.vocab, n))
         done += n
 lane.wait()
+if level:  # decode on a green-context partition of level*16 SMs, as the AgentServe engine does
+    slots = Slots(0, levels=9, granularity=16)
+    dstream, _ = slots.bind(level)
+    lane.set_stream(dstream)
+    lane.set_sms(slots.sm_counts(level)[0])
 steps = 2 if ncu else 20
 times = []
 for i in range(steps):
@@ -45,5 +52,15 @@ for i in range(steps):
         torch.cuda.nvtx.range_pop()
     times.append((t1 - t0, t2 - t0, lane.last_ms()))
 t = np.array(times[3:] if not ncu else times)
-print(f"{name} B={B} ctx={ctx}: host enqueue {1e3*np.median(t[:,0]):.3f} ms, wall {1e3*np.median(t[:,1]):.3f} ms, "
+lane_sms = slots.sm_counts(level)[0] if level else 148
+if "--prof" in sys.argv:  # per-category device time, one CUDA-event pair per launch (no PDL)
+    lane.profile(True)
+    lane.stats(reset=True)
+    for _ in range(5):
+        lane.forward(kv, [(s, 1, 1) for s in range(B)], rng.integers(0, m.vocab, B))
+        lane.wait()
+    st = lane.stats(reset=True)
+    lane.profile(False)
+    print("  per step:", {k: f"{v[0]/5*1000:.0f}us/{v[2]//5}" for k, v in st.items() if v[2]})
+print(f"{name} B={B} ctx={ctx} sms={lane_sms}: host enqueue {1e3*np.median(t[:,0]):.3f} ms, wall {1e3*np.median(t[:,1]):.3f} ms, "
       f"lane event {np.median(t[:,2]):.3f} ms")
