@@ -91,9 +91,13 @@ __global__ void __launch_bounds__(WARPS * 32, (DgCfg<NT, WARPS>::kMinBlocks)) dg
     // rows of this warp: consecutive 16-row slabs, except for the fused RoPE epilogue, where a
     // CTA (RW = 2) owns slab c of the first half of head `hq_` and the same slab of the second
     // half, so every rotate_half pair (j, j + hd/2) is reduced inside the CTA
+    // (RW/2 pairs per CTA: warp rw serves half rw % 2 of pair unit blockIdx.x * RW/2 + rw / 2)
     const int spp = p.epi == EPI_QKV ? p.rope.hd / 32 : 1;  // slabs per half head
-    const int head_ = blockIdx.x / spp, slab_ = blockIdx.x % spp;
-    const int r0 = p.epi == EPI_QKV ? head_ * p.rope.hd + rw * (p.rope.hd / 2) + 16 * slab_ : row_cta + 16 * rw;
+    const int unit_ = blockIdx.x * (RW / 2) + rw / 2;
+    const int head_ = unit_ / spp, slab_ = unit_ % spp;
+    const int r0 = p.epi == EPI_QKV ? (unit_ < p.n_out / 32 ? head_ * p.rope.hd + (rw & 1) * (p.rope.hd / 2) + 16 * slab_
+                                                            : p.rows_pad)
+                                    : row_cta + 16 * rw;
     const int KB = p.K / 64;
     const bool rows_ok = r0 < p.rows_pad;
     const int nk = rows_ok && kw < KB ? (KB - kw + KW - 1) / KW : 0;
@@ -230,34 +234,36 @@ __global__ void __launch_bounds__(WARPS * 32, (DgCfg<NT, WARPS>::kMinBlocks)) dg
         break;
     }
     case EPI_QKV: {
-        // pair-slab CTA: red rows [0,16) = features f1 = head*hd + 16c + j of the first half,
-        // rows [16,32) = f1 + hd/2.  q/k heads rotate the pair, v heads copy it.
+        // pair-slab CTA: red rows [32 pi, 32 pi + 16) = features f1 = head*hd + 16c + j of the
+        // first half of pair unit pi, rows [32 pi + 16, 32 pi + 32) = f1 + hd/2.  q/k heads
+        // rotate the pair, v heads copy it.
         const RopeEpi& Rp = p.rope;
         const int hd = Rp.hd, H = hd / 2, qd = Rp.hq * hd, kvd = Rp.hkv * hd;
-        const int f0 = head_ * hd;
-        if (f0 < p.n_out) {
-            for (int e = threadIdx.x; e < 16 * T; e += kThreadsG) {
-                const int j = 16 * slab_ + (e & 15), tok = e >> 4;
-                const int sl = Rp.slot[tok];
-                float x1 = sum(e & 15, tok), x2 = sum(16 + (e & 15), tok);
-                if (p.bias) {
-                    x1 += __bfloat162float(p.bias[f0 + j]);
-                    x2 += __bfloat162float(p.bias[f0 + j + H]);
-                }
-                if (f0 >= qd + kvd) {
-                    __nv_bfloat16* v = Rp.v_pool + pool_off(Rp, sl, (f0 - qd - kvd) / hd);
-                    v[j] = __float2bfloat16_rn(x1);
-                    v[j + H] = __float2bfloat16_rn(x2);
-                    continue;
-                }
-                const int pos = Rp.pos[tok];
-                float y1, y2;
-                rope2(bf16r(x1), bf16r(x2), Rp.cos_t[(size_t)pos * H + j], Rp.sin_t[(size_t)pos * H + j], y1, y2);
-                __nv_bfloat16* dst = f0 < qd ? Rp.q_out + ((size_t)tok * Rp.hq + f0 / hd) * hd
-                                             : Rp.k_pool + pool_off(Rp, sl, (f0 - qd) / hd);
-                dst[j] = __float2bfloat16_rn(y1);
-                dst[j + H] = __float2bfloat16_rn(y2);
+        const int P = RW / 2;
+        for (int e = threadIdx.x; e < P * 16 * T; e += kThreadsG) {
+            const int jj = e & 15, pi = (e >> 4) % P, tok = (e >> 4) / P;
+            const int u = blockIdx.x * P + pi;
+            if (u >= p.n_out / 32) continue;
+            const int f0 = (u / spp) * hd, j = 16 * (u % spp) + jj;
+            const int sl = Rp.slot[tok];
+            float x1 = sum(32 * pi + jj, tok), x2 = sum(32 * pi + 16 + jj, tok);
+            if (p.bias) {
+                x1 += __bfloat162float(p.bias[f0 + j]);
+                x2 += __bfloat162float(p.bias[f0 + j + H]);
             }
+            if (f0 >= qd + kvd) {
+                __nv_bfloat16* v = Rp.v_pool + pool_off(Rp, sl, (f0 - qd - kvd) / hd);
+                v[j] = __float2bfloat16_rn(x1);
+                v[j + H] = __float2bfloat16_rn(x2);
+                continue;
+            }
+            const int pos = Rp.pos[tok];
+            float y1, y2;
+            rope2(bf16r(x1), bf16r(x2), Rp.cos_t[(size_t)pos * H + j], Rp.sin_t[(size_t)pos * H + j], y1, y2);
+            __nv_bfloat16* dst = f0 < qd ? Rp.q_out + ((size_t)tok * Rp.hq + f0 / hd) * hd
+                                         : Rp.k_pool + pool_off(Rp, sl, (f0 - qd) / hd);
+            dst[j] = __float2bfloat16_rn(y1);
+            dst[j + H] = __float2bfloat16_rn(y2);
         }
         break;
     }
@@ -311,19 +317,24 @@ int dgemv_max_tokens() { return 32; }
 cudaError_t dgemv_launch(DgemvParams p, int num_sms, cudaStream_t stream) {
     if (p.T < 1 || p.T > 32 || p.K % 64 != 0) return cudaErrorInvalidValue;
     if (p.epi == EPI_QKV && (p.rope.hd % 32 != 0 || p.n_out % p.rope.hd != 0)) return cudaErrorInvalidValue;
-    // Row-warps per CTA: a pair of half-head slabs for the fused RoPE epilogue; otherwise as
-    // many 16-row slabs per CTA as still leave >= 2 CTAs per SM (fewer X re-reads).  A grid
-    // that does not fill the SMs gets 16 warps per CTA (twice the K split, half the depth).
+    // Rows per CTA: the fewest (most CTAs, least weight per SM) that still fit ONE wave of
+    // resident CTAs -- a second partial wave doubles the latency of these launch-bound
+    // projections on a small Green Context partition.  Fused RoPE: pairs of half-head slabs.
     const int tiles16 = (p.n_out + 15) / 16;
+    const int slots = num_sms * ((p.T + 7) / 8 <= 2 ? 2 : 1);
     int rw = 1, grid = 0;
     if (p.epi == EPI_QKV) {
-        rw = 2;
-        grid = p.n_out / 32;
+        const int pairs = p.n_out / 32;
+        int P = 1;
+        while (P < 4 && (pairs + P - 1) / P > slots) P *= 2;
+        rw = 2 * P;
+        grid = (pairs + P - 1) / P;
     } else {
-        while (rw < 8 && (tiles16 / (2 * rw)) >= 2 * num_sms) rw *= 2;
+        while (rw < 8 && (tiles16 + rw - 1) / rw > slots) rw *= 2;
         grid = (p.n_out + 16 * rw - 1) / (16 * rw);
     }
     p.rw = rw;
+    // a grid that does not fill the SMs gets 16 warps per CTA (twice the K split)
     if (grid <= num_sms) return launch_w<16>(p, grid, stream);
     return launch_w<8>(p, grid, stream);
 }

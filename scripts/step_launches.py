@@ -21,11 +21,13 @@ ctx = int(args[2]) if len(args) > 2 else 2048
 ncu = "--ncu" in sys.argv
 level = int([a for a in sys.argv if a.startswith("--level=")][0].split("=")[1]) if any(
     a.startswith("--level=") for a in sys.argv) else 0
-m = Model(name, seed=13, max_context=ctx + 256)
-kv = KvPool(m, num_blocks=B * ((ctx + 63) // 64 + 2) + 8)
+chunk = int([a for a in sys.argv if a.startswith("--chunk=")][0].split("=")[1]) if any(
+    a.startswith("--chunk=") for a in sys.argv) else 0  # admitted resume chunk rows per step
+m = Model(name, seed=13, max_context=ctx + 256 + 30 * chunk)
+kv = KvPool(m, num_blocks=(B + 1) * ((ctx + 30 * chunk + 63) // 64 + 2) + 8)
 lane = Lane(m, max_tokens=2048, max_segments=B + 4)
 rng = np.random.default_rng(0)
-for s in range(B):
+for s in range(B + (1 if chunk else 0)):
     done = 0
     while done < ctx - 1:
         n = min(2048, ctx - 1 - done)
@@ -44,7 +46,9 @@ for i in range(steps):
     if ncu and i == steps - 1:
         torch.cuda.nvtx.range_push("step")
     t0 = time.perf_counter()
-    lane.forward(kv, [(s, 1, 1) for s in range(B)], toks)
+    segs = [(s, 1, 1) for s in range(B)] + ([(B, chunk, 1)] if chunk else [])
+    toks = np.concatenate([toks, rng.integers(0, m.vocab, chunk)]) if chunk else toks
+    lane.forward(kv, segs, toks)
     t1 = time.perf_counter()
     lane.wait()
     t2 = time.perf_counter()
@@ -57,10 +61,11 @@ if "--prof" in sys.argv:  # per-category device time, one CUDA-event pair per la
     lane.profile(True)
     lane.stats(reset=True)
     for _ in range(5):
-        lane.forward(kv, [(s, 1, 1) for s in range(B)], rng.integers(0, m.vocab, B))
+        segs = [(s, 1, 1) for s in range(B)] + ([(B, chunk, 1)] if chunk else [])
+        lane.forward(kv, segs, rng.integers(0, m.vocab, B + chunk))
         lane.wait()
     st = lane.stats(reset=True)
     lane.profile(False)
     print("  per step:", {k: f"{v[0]/5*1000:.0f}us/{v[2]//5}" for k, v in st.items() if v[2]})
-print(f"{name} B={B} ctx={ctx} sms={lane_sms}: host enqueue {1e3*np.median(t[:,0]):.3f} ms, wall {1e3*np.median(t[:,1]):.3f} ms, "
+print(f"{name} B={B}+{chunk} ctx={ctx} sms={lane_sms}: host enqueue {1e3*np.median(t[:,0]):.3f} ms, wall {1e3*np.median(t[:,1]):.3f} ms, "
       f"lane event {np.median(t[:,2]):.3f} ms")
