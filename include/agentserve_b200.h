@@ -173,6 +173,10 @@ asb_status asb_debug_gemm_timeline(asb_lane* lane, unsigned long long* out, int 
 /* ASB_MK_TIMELINE=1 at lane creation: globaltimer (ns) at the start of every phase of the
  * lane's most recent persistent decode-step launch, [num_sms][256] (slot 255 = CTA exit). */
 asb_status asb_debug_mk_timeline(asb_lane* lane, unsigned long long* out, int n);
+/* ASB_ATTN_TIMELINE=1 at lane creation: per-CTA globaltimer stamps [1024][8] of the last decode
+ * attention launch of the lane's most recent forward (entry, after pdl wait, first K/V
+ * sub-block, consumers done, partial written, exit). */
+asb_status asb_debug_attn_timeline(asb_lane* lane, unsigned long long* out, int n);
 asb_status asb_debug_gemm(const void* x, const void* w, const void* bias, const void* resid,
                           void* out, int tokens, int n_out, int k, int epi, int force_path,
                           int splits, void* stream);

@@ -36,6 +36,7 @@ struct AttnShape {
     int num_blocks;   // blocks per layer in the pool
     int layer;        // layer index (selects the pool slice)
     float scale_log2; // log2(e) / sqrt(hd)
+    unsigned long long* dbg = nullptr;  // decode attention: per-CTA globaltimer stamps [cta][8]
 };
 
 // grid = (items, hkv, splits).  Split-KV over gridDim.z when the grid is small (resume

@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                        const __nv_bfloat16* __restrict__ q, const DecodeItem* __restrict__ items,
                        const int32_t* __restrict__ tables, __nv_bfloat16* __restrict__ out,
                        float* __restrict__ part_o, float* __restrict__ part_ml,
-                       int* __restrict__ counters, int subs_per_split, int n_stages, AttnShape s) {
+                       int* __restrict__ counters, int subs_per_split, int n_stages, int cluster_merge,
+                       AttnShape s) {
     using C = DC<HD>;
     constexpr int NT = HD / 8;  // O n-tiles (8 dims each)
     const int kWarpsR = blockDim.x / 32 - 1;  // consumer warps
@@ -78,6 +79,15 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     uint64_t* full = reinterpret_cast<uint64_t*>(mls + kWarpsR * 16);
     uint64_t* empty = full + kStagesR;
 
+    const int cta_id = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    auto stamp = [&](int k) {
+        if (s.dbg && cta_id < 1024) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            s.dbg[cta_id * 8 + k] = t;
+        }
+    };
+    if (threadIdx.x == 0) stamp(0);
     const DecodeItem it = items[blockIdx.x];
     const int kvh = blockIdx.y;
     const int G = s.hq / s.hkv;
@@ -98,13 +108,21 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     }
     __syncthreads();
     pdl_trigger();
-    pdl_wait();  // q and the appended K/V come from the kernel before us
 
     if (warp == kWarpsR) {
         // ------------------------------------------------------------ producer
+        // K/V of positions before this step's token were written by earlier steps: stream them
+        // while the kernel before us (the QKV projection appending the new token) is still
+        // running, and wait for it only before the sub-block that holds the new token.
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
+            const int new_sub = (it.ctx_len - 1) / kSub;
+            bool waited = false;
             for (int i = 0; i < n_local; ++i) {
+                if (!waited && s0 + i >= new_sub) {
+                    pdl_wait();
+                    waited = true;
+                }
                 const int st = stage_of(i, kWarpsR, kStagesR);
                 mbar_wait(&empty[st], ((i / kStagesR) & 1) ^ 1);
                 mbar_expect_tx(&full[st], C::kStage);
@@ -119,11 +137,14 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                     tma_load_2d_hint(vd + h * (kSub * 128), &tmap_v, &full[st], h * 64, row, pol);
                 }
             }
+            if (!waited) pdl_wait();
         }
         return;
     }
 
     // ---------------------------------------------------------------- consumers
+    pdl_wait();  // q comes from the kernel before us
+    if (threadIdx.x == 0) stamp(1);
     const int g = lane >> 2, t = lane & 3;  // fragment row / column-pair owner
     // Q A-fragments (rows = heads): (row g, k 2t..2t+1) and (row g, k 2t+8..2t+9); the
     // fragment registers of rows g+8 and of rows >= G are zero
@@ -148,6 +169,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     for (int i = warp; i < n_local; i += kWarpsR) {
         const int st = stage_of(i, kWarpsR, kStagesR);
         mbar_wait(&full[st], (i / kStagesR) & 1);
+        if (i == 0 && lane == 0) stamp(2);
         const uint32_t kt = smem_u32(ring + st * C::kStage);
         const uint32_t vt = kt + C::kTile;
         // ---- S = Q K^T : 4 n-tiles of 8 keys
@@ -220,6 +242,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     }
 
     // ---------------------------------------------------------------- merge warps
+    if (threadIdx.x == 0) stamp(3);
     float* mw = mrg + warp * 8 * HD;
     if (g < G) {
 #pragma unroll
@@ -234,6 +257,11 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     }
     named_sync(1, kWarpsR * 32);
     const bool single = gridDim.z == 1;
+    const bool cmerge = !single && cluster_merge;
+    // cluster merge: this CTA's (M, L, O) parked at the start of the drained ring
+    float* cO = reinterpret_cast<float*>(ring);  // [G][HD]
+    float* cM = cO + 8 * HD;                     // [G]
+    float* cL = cM + 8;                          // [G]
     for (int e = threadIdx.x; e < G * HD; e += kWarpsR * 32) {
         const int h = e / HD, d = e % HD;
         float M = -FLT_MAX;
@@ -251,6 +279,12 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         const int hh = kvh * G + h;
         if (single) {
             out[(size_t)it.q_row * s.hq * HD + hh * HD + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+        } else if (cmerge) {
+            cO[h * HD + d] = O;
+            if (d == 0) {
+                cM[h] = M;
+                cL[h] = L;
+            }
         } else {
             const size_t slot = ((size_t)blockIdx.x * s.hq + hh) * gridDim.z + blockIdx.z;
             part_o[slot * HD + d] = O;
@@ -260,7 +294,50 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             }
         }
     }
-    if (single) return;
+    if (single) {
+        if (threadIdx.x == 0) stamp(5);
+        return;
+    }
+    if (cmerge) {
+        // ---------------------------------------------------------- cluster split merge
+        // The S splits of this (row, kv head) are the S CTAs of one thread-block cluster: after
+        // a cluster barrier, CTA rank r merges slice r of the G x HD outputs straight from its
+        // peers' shared memory (DSMEM), in split order -- the arithmetic of
+        // decode_combine_kernel, with no global partials, fences or atomics.
+        cluster_sync();
+        if (threadIdx.x == 0) stamp(4);
+        const int S = gridDim.z, r = blockIdx.z;
+        const int n = G * HD, lo = (n * r) / S, hi = (n * (r + 1)) / S;
+        const uint32_t bO = smem_u32(cO), bM = smem_u32(cM), bL = smem_u32(cL);
+        for (int e = lo + threadIdx.x; e < hi; e += kWarpsR * 32) {
+            const int h = e / HD, d = e % HD;
+            float mq[8], lq[8], oq[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q < S) {
+                    mq[q] = ld_dsmem_f32(mapa_shared(bM + 4 * h, q));
+                    lq[q] = ld_dsmem_f32(mapa_shared(bL + 4 * h, q));
+                    oq[q] = ld_dsmem_f32(mapa_shared(bO + 4 * e, q));
+                }
+            }
+            float M = -FLT_MAX;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < S) M = fmaxf(M, mq[q]);
+            float L = 0.f, O = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q >= S || lq[q] == 0.f) continue;
+                const float w = exp2f(mq[q] - M);
+                L += lq[q] * w;
+                O += oq[q] * w;
+            }
+            out[(size_t)it.q_row * s.hq * HD + (kvh * G + h) * HD + d] = __float2bfloat16_rn(O / L);
+        }
+        cluster_sync();  // peers may still be reading this CTA's partial
+        if (threadIdx.x == 0) stamp(5);
+        return;
+    }
     // ---------------------------------------------------------------- split merge
     // Last-arriving split of this (row, kv head) merges all splits in split order (the same
     // arithmetic as decode_combine_kernel: deterministic), then re-arms the counter.
@@ -274,6 +351,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         if (last_s) *cnt = 0;
     }
     named_sync(1, kWarpsR * 32);
+    if (threadIdx.x == 0) stamp(4);
     if (!last_s) return;
     __threadfence();
     // per (head, split) weight exp2(m - M) and the normaliser L, once per head, in smem (the
@@ -318,6 +396,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         }
         out[(size_t)it.q_row * s.hq * HD + hh * HD + d] = __float2bfloat16_rn(O / linv[h]);
     }
+    if (threadIdx.x == 0) stamp(5);
 }
 
 // Merge split partials -> normalised bf16 output.  grid = (n_items, hq), block = HD.
@@ -360,8 +439,35 @@ cudaError_t launch_hd(const CUtensorMap& tk, const CUtensorMap& tv, const __nv_b
         attr = true;
     }
     dim3 grid(n_items, s.hkv, splits);
-    cudaError_t e = launch_k(decode_attn_kernel<HD>, grid, dim3((warps + 1) * 32), smem, st, tk, tv, q, items,
-                             tables, out, po, pml, cnt, sps, stages, s);
+    // splits <= 8: one thread-block cluster per (row, kv head), merged over DSMEM
+    static const bool no_cluster = std::getenv("ASB_ATTN_NO_CLUSTER") != nullptr;
+    const int cmerge = (splits > 1 && splits <= 8 && !no_cluster) ? 1 : 0;
+    cudaError_t e;
+    if (cmerge) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3((warps + 1) * 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute a[2];
+        a[0].id = cudaLaunchAttributeClusterDimension;
+        a[0].val.clusterDim.x = 1;
+        a[0].val.clusterDim.y = 1;
+        a[0].val.clusterDim.z = splits;
+        int na = 1;
+        if (tl_pdl) {
+            a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            a[1].val.programmaticStreamSerializationAllowed = 1;
+            na = 2;
+        }
+        cfg.attrs = a;
+        cfg.numAttrs = na;
+        e = cudaLaunchKernelEx(&cfg, decode_attn_kernel<HD>, tk, tv, q, items, tables, out, po, pml, cnt, sps,
+                               stages, cmerge, s);
+        return e;
+    }
+    e = launch_k(decode_attn_kernel<HD>, grid, dim3((warps + 1) * 32), smem, st, tk, tv, q, items,
+                 tables, out, po, pml, cnt, sps, stages, 0, s);
     if (e == cudaSuccess && splits > 1 && !cnt)
         e = launch_k(decode_combine_kernel<HD>, dim3(n_items, s.hq), dim3(HD), 0, st, items,
                      static_cast<const float*>(po), static_cast<const float*>(pml), splits, out, s.hq);
@@ -387,7 +493,9 @@ cudaError_t decode_attention(const CUtensorMap& tmap_k32, const CUtensorMap& tma
                              const AttnShape& s, cudaStream_t stream) {
     if (n_items <= 0) return cudaSuccess;
     if (s.hq / s.hkv > 8) return cudaErrorInvalidValue;
-    const int splits0 = decode_splits(n_items, s.hkv, max_ctx, num_sms, max_splits);
+    // the cluster merge (launch_hd) takes up to 8 splits: a portable cluster
+    static const bool no_cluster = std::getenv("ASB_ATTN_NO_CLUSTER") != nullptr;
+    const int splits0 = decode_splits(n_items, s.hkv, max_ctx, num_sms, no_cluster ? max_splits : std::min(max_splits, 8));
     const int subs = (max_ctx + kSub - 1) / kSub;
     const int sps = (subs + splits0 - 1) / splits0;
     const int splits = (subs + sps - 1) / sps;

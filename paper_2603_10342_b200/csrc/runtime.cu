@@ -283,6 +283,7 @@ struct asb_lane {
     int* mk_acnt = nullptr;
     int mk_max_spl = 16;
     unsigned long long* mk_dbg = nullptr;  // ASB_MK_TIMELINE=1: per-CTA phase start stamps
+    unsigned long long* attn_dbg = nullptr;  // ASB_ATTN_TIMELINE=1: decode-attention CTA stamps
     bool mega = std::getenv("ASB_MEGA") != nullptr && std::atoi(std::getenv("ASB_MEGA")) != 0;  // opt-in
     CUtensorMap map_x[5];
     bool pdl = std::getenv("ASB_NO_PDL") == nullptr;  // programmatic dependent launch
@@ -837,6 +838,10 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
             cuda_check(cudaMemset(L->mk_bar, 0, 256), "mk");
             cuda_check(cudaMemset(L->mk_tile_cnt, 0, size_t(max_n / 128 + 2) * 4), "mk");
             cuda_check(cudaMemset(L->mk_acnt, 0, size_t(rows) * s.hkv * 4), "mk");
+            if (std::getenv("ASB_ATTN_TIMELINE")) {
+                L->attn_dbg = static_cast<unsigned long long*>(dmalloc(1024 * 8 * 8, L->allocs));
+                cuda_check(cudaMemset(L->attn_dbg, 0, 1024 * 8 * 8), "attn dbg");
+            }
             if (std::getenv("ASB_MK_TIMELINE")) {
                 L->mk_dbg = static_cast<unsigned long long*>(
                     dmalloc(size_t(m->num_sms) * kMkDbgSlots * 8, L->allocs));
@@ -993,6 +998,10 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         as.hd = s.hd;
         as.num_blocks = kv->nb;
         as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(s.hd)));
+        if (L->attn_dbg) {
+            cuda_check(cudaMemsetAsync(L->attn_dbg, 0, 1024 * 8 * 8, L->stream), "attn dbg");
+            as.dbg = L->attn_dbg;
+        }
         // algorithmic work per layer: decode attention streams every context token's K and V
         // once; prefill attention is 4*hd flops per (query, key<=query) pair per head.
         double dattn_bytes = 0.0, pattn_flops = 0.0;
@@ -1198,6 +1207,16 @@ asb_status asb_debug_mk_timeline(asb_lane* L, unsigned long long* out, int n) {
         cuda_check(cudaStreamSynchronize(L->stream), "sync");
         const size_t total = size_t(L->m->num_sms) * kMkDbgSlots;
         cuda_check(cudaMemcpy(out, L->mk_dbg, std::min<size_t>(total, size_t(n)) * 8, cudaMemcpyDeviceToHost),
+                   "timeline");
+    });
+}
+
+asb_status asb_debug_attn_timeline(asb_lane* L, unsigned long long* out, int n) {
+    if (!L || !out) return ASB_ERR_INVALID_ARGUMENT;
+    return guarded([&] {
+        if (!L->attn_dbg) fail(ASB_ERR_NO_DATA, "lane created without ASB_ATTN_TIMELINE=1");
+        cuda_check(cudaStreamSynchronize(L->stream), "sync");
+        cuda_check(cudaMemcpy(out, L->attn_dbg, std::min<size_t>(1024 * 8, size_t(n)) * 8, cudaMemcpyDeviceToHost),
                    "timeline");
     });
 }
