@@ -268,7 +268,20 @@ __global__ void __launch_bounds__(WARPS * 32, (DgCfg<NT, WARPS>::kMinBlocks)) dg
         break;
     }
     default: {
-        for (int e = threadIdx.x; e < R * T; e += kThreadsG) {
+        // <= 16 elements per thread (R x T <= 128 x 32 over >= 256 threads); residual loads all
+        // issued before the first (possibly aliasing, in-place) store
+        float rv[16];
+        if (p.epi == EPI_RESID) {
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int e = threadIdx.x + u * kThreadsG, rl = e % R, tok = e / R, n = row_cta + rl;
+                rv[u] = (e < R * T && n < p.n_out) ? __bfloat162float(p.resid[(size_t)tok * p.ldr + n]) : 0.f;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int e = threadIdx.x + u * kThreadsG;
+            if (e >= R * T) break;
             const int rl = e % R, tok = e / R;
             const int n = row_cta + rl;
             if (n >= p.n_out) continue;
@@ -281,7 +294,7 @@ __global__ void __launch_bounds__(WARPS * 32, (DgCfg<NT, WARPS>::kMinBlocks)) dg
                     if (k) atomicMax(&key_s[tok], k);
                 }
             } else {
-                if (p.epi == EPI_RESID) v += __bfloat162float(p.resid[(size_t)tok * p.ldr + n]);
+                if (p.epi == EPI_RESID) v += rv[u];
                 else if (p.bias) v += __bfloat162float(p.bias[n]);
                 p.out[o] = __float2bfloat16_rn(v);
             }

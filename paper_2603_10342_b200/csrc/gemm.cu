@@ -510,9 +510,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 } else {
-                    // swap: D[m = weight row][n = token] -> Y[token][weight row]
+                    // swap: D[m = weight row][n = token] -> Y[token][weight row].  Residual: all
+                    // 32 loads first (the in-place store would otherwise serialise them)
+                    if (p.epi == EPI_RESID) {
+                        float rv[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) epi.store(n0 + j, m, __uint_as_float(r[j]));
+                        for (int j = 0; j < 32; ++j)
+                            rv[j] = (n0 + j < p.tokens && m < p.n_out)
+                                        ? __bfloat162float(p.resid[static_cast<size_t>(n0 + j) * p.ldr + m]) : 0.f;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (n0 + j < p.tokens && m < p.n_out)
+                                p.out[static_cast<size_t>(n0 + j) * p.ldo + m] =
+                                    __float2bfloat16_rn(__uint_as_float(r[j]) + rv[j]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) epi.store(n0 + j, m, __uint_as_float(r[j]));
+                    }
                     if (p.amax) {
                         // fused greedy sample: key[j] per lane, then a butterfly reduce-scatter
                         // leaves lane l with the max over the warp's 32 rows for token n0 + l
@@ -547,18 +561,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Reduce the tile over the cluster: CTA `rank` finishes row pairs
         // [64*rank/S, 64*(rank+1)/S), summing the S partials in rank order.
         cluster_sync();
+        if (threadIdx.x == 0) stamp(7);
         const int S = p.splits > 1 ? p.splits : 1;
         const int rank = blockIdx.x % S;
         const int tile = blockIdx.x / S;
         const uint32_t base = smem_u32(part);
-        auto sum2 = [&](int tok, int row) {
+        auto sum2 = [&](int tok, int row) {  // all S loads in flight, then the sum in rank order
             const uint32_t off = base + static_cast<uint32_t>((tok * BM + row) * 4);
+            float2 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < S) v[q] = ld_dsmem_f2(mapa_shared(off, q));
             float2 acc = make_float2(0.f, 0.f);
-            for (int q = 0; q < S; ++q) {
-                const float2 v = ld_dsmem_f2(mapa_shared(off, q));
-                acc.x += v.x;
-                acc.y += v.y;
-            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < S) {
+                    acc.x += v[q].x;
+                    acc.y += v[q].y;
+                }
             return acc;
         };
         if (p.epi == EPI_QKV) {
@@ -615,16 +635,67 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int p0 = (64 * rank) / S, p1 = (64 * (rank + 1)) / S, np = p1 - p0;
         Epi epi{p};
-        for (int e = threadIdx.x; e < np * p.tokens; e += kThreads) {
-            const int tok = e / np;
-            const int row = 2 * (p0 + e % np);
-            const float2 acc = sum2(tok, row);
-            const int m = (tile % tiles_m) * BM + row;
-            epi.store_pair(tok, m, acc.x, acc.y);
-            if (p.amax && m < p.n_out) {
-                unsigned long long k = argmax_key(acc.x, m);
-                if (m + 1 < p.n_out) k = max(k, argmax_key(acc.y, m + 1));
-                if (k) atomicMax(p.amax + tok, k);
+        // CH elements per thread per round: every DSMEM partial and residual load of the round
+        // is issued before the first sum (a per-element load -> add -> store chain would
+        // serialise ~S+1 round trips per element, and the in-place residual store keeps the
+        // compiler from hoisting the next residual load)
+        constexpr int CH = 4;
+        for (int e0 = threadIdx.x; e0 < np * p.tokens; e0 += kThreads * CH) {
+            float2 v[CH][8];
+            float2 rr[CH];
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int e = e0 + c * kThreads;
+                rr[c] = make_float2(0.f, 0.f);
+                if (e >= np * p.tokens) continue;
+                const int tok = e / np, row = 2 * (p0 + e % np);
+                const uint32_t off = base + static_cast<uint32_t>((tok * BM + row) * 4);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q < S) v[c][q] = ld_dsmem_f2(mapa_shared(off, q));
+                const int m = (tile % tiles_m) * BM + row;
+                if (p.epi == EPI_RESID && m < p.n_out) {
+                    const __nv_bfloat16* rp = p.resid + static_cast<size_t>(tok) * p.ldr + m;
+                    if (m + 1 < p.n_out && (p.ldr & 1) == 0) {
+                        const uint32_t w2 = *reinterpret_cast<const uint32_t*>(rp);
+                        rr[c] = make_float2(bf16_lo(w2), bf16_hi(w2));
+                    } else {
+                        rr[c] = make_float2(__bfloat162float(rp[0]), m + 1 < p.n_out ? __bfloat162float(rp[1]) : 0.f);
+                    }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int e = e0 + c * kThreads;
+                if (e >= np * p.tokens) continue;
+                const int tok = e / np, row = 2 * (p0 + e % np);
+                float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q < S) {
+                        acc.x += v[c][q].x;
+                        acc.y += v[c][q].y;
+                    }
+                const int m = (tile % tiles_m) * BM + row;
+                if (p.epi == EPI_RESID) {
+                    if (tok < p.tokens && m < p.n_out) {
+                        const size_t o = static_cast<size_t>(tok) * p.ldo + m;
+                        const float y0 = acc.x + rr[c].x, y1 = acc.y + rr[c].y;
+                        if (m + 1 < p.n_out && (p.ldo & 1) == 0) {
+                            *reinterpret_cast<uint32_t*>(p.out + o) = pack_bf16(y0, y1);
+                        } else {
+                            p.out[o] = __float2bfloat16_rn(y0);
+                            if (m + 1 < p.n_out) p.out[o + 1] = __float2bfloat16_rn(y1);
+                        }
+                    }
+                } else {
+                    epi.store_pair(tok, m, acc.x, acc.y);
+                }
+                if (p.amax && m < p.n_out) {
+                    unsigned long long k = argmax_key(acc.x, m);
+                    if (m + 1 < p.n_out) k = max(k, argmax_key(acc.y, m + 1));
+                    if (k) atomicMax(p.amax + tok, k);
+                }
             }
         }
         cluster_sync();  // peers may still be reading our partial

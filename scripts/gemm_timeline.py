@@ -33,10 +33,8 @@ for name, N, K, epi in shapes:
     check(L.asb_debug_gemm_timeline(None, buf, 148 * 8))
     t = np.array(buf[:], dtype=np.float64).reshape(148, 8)
     t = t[t[:, 0] > 0]
-    print("epilogue threads done at CTA barrier:", sorted(set(t[:, 7].astype(int).tolist())))
     rel = (t - t[:, 0].min()) / 1000.0
-    rel[:, 7] = 0
     f = lambda c: "%6.1f/%6.1f/%6.1f" % (rel[:, c].min(), np.median(rel[:, c]), rel[:, c].max())
     print(f"{name:8s} T={T} N={N} K={K} ctas={len(t)}  start {f(0)} tmem {f(6)} 1st-data {f(4)}  mma {f(1)} "
-          f"1st-acc {f(5)}  epi {f(2)}  exit {f(3)}  "
+          f"1st-acc {f(5)}  epi {f(2)}  cluster-sync {f(7)}  exit {f(3)}  "
           f"min-bytes-time {N*K*2/6.55e3/1e3:.1f}us")
