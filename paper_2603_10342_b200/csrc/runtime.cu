@@ -849,7 +849,7 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
             }
         }
         // split-KV partials for small prefill grids (resume chunks): <= 4096 rows of 128 queries
-        L->ppart_rows = size_t(4096) * 256 / 16;
+        L->ppart_rows = size_t(4096) * 256 / 4;
         L->ppart_o = static_cast<float*>(dmalloc(L->ppart_rows * s.hd * 4, L->allocs));
         L->ppart_ml = static_cast<float*>(dmalloc(L->ppart_rows * 2 * 4, L->allocs));
         L->meta_ints = size_t(3) * T + L->max_segs + L->max_tbl + 4 * size_t(L->max_segs) +
@@ -1005,9 +1005,11 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         // algorithmic work per layer: decode attention streams every context token's K and V
         // once; prefill attention is 4*hd flops per (query, key<=query) pair per head.
         double dattn_bytes = 0.0, pattn_flops = 0.0;
-        const int psplits = pitems.empty() ? 1
-                                           : prefill_splits(int(pitems.size()), s.hkv, max_pblocks,
-                                                            L->n_sms(), L->ppart_rows);
+        static const int psplit_env = std::getenv("ASB_PREFILL_SPLITS") ? std::atoi(std::getenv("ASB_PREFILL_SPLITS")) : 0;
+        int psplits = pitems.empty() ? 1
+                                     : prefill_splits(int(pitems.size()), s.hkv, max_pblocks, L->n_sms(), L->ppart_rows);
+        if (psplit_env > 0 && !pitems.empty())  // timing experiments: force the split count
+            psplits = std::max(1, std::min({psplit_env, 32, int(L->ppart_rows / (pitems.size() * s.hkv * 256))}));
         for (const auto& it : ditems) dattn_bytes += double(it.ctx_len) * s.hkv * s.hd * 2 * 2;
         for (const auto& it : pitems)
             pattn_flops += 4.0 * s.hd * s.hq *
