@@ -45,11 +45,16 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int kThreads = 192;
 
-template <int BN>
+// KP = 64-wide k-blocks per pipeline stage.  The decode (swap) path at BN <= 64 uses KP = 2:
+// one 32 KiB weight box + one activation box per stage.  TMA throughput per SM is set by the
+// request size more than by the requests in flight (scripts/probes/stream.cu on a 16-SM
+// partition: 16 KiB requests ~90 GB/s/SM, 32 KiB ~150), and a decode step on a small Green
+// Context partition is exactly that per-SM stream.
+template <int BN, int KP = 1>
 struct GemmCfg {
-    static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
-    static constexpr int kBytesA = BM * BK * 2;
-    static constexpr int kBytesB = BN * BK * 2;
+    static constexpr int kStages = KP == 2 ? (BN <= 32 ? 5 : 4) : (BN >= 256 ? 4 : (BN >= 128 ? 6 : 8));
+    static constexpr int kBytesA = BM * BK * 2 * KP;
+    static constexpr int kBytesB = BN * BK * 2 * KP;
     static constexpr int kStageBytes = kBytesA + kBytesB;
     static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : 2 * BN;  // power of two >= 32
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
@@ -166,11 +171,11 @@ struct Work {
     }
 };
 
-template <int BN>
+template <int BN, int KP>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const GemmParams p) {
-    using C = GemmCfg<BN>;
+    using C = GemmCfg<BN, KP>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int tiles_m = (p.M + BM - 1) / BM;
     const int tiles_n = (p.N + BN - 1) / BN;
-    const int k_blocks = (p.K + BK - 1) / BK;
+    const int k_blocks = ((p.K + BK - 1) / BK + KP - 1) / KP;  // pipeline k-units of KP blocks
 
     if (warp == 0) {
         if (elect_one()) {
@@ -235,8 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // Weight operand: A in swap, B in normal.  Activations: the other one.
             auto load_w = [&](int stage, int kb, int tm, int tn) {
                 if (p.swap) {
-                    if (p.a_packed)
-                        tma_load_4d_hint(smem_a + stage * C::kBytesA, &tmap_a, &full_bar[stage], 0, 0, kb, tm, pol_w);
+                    if (p.a_packed)  // box = KP consecutive k-blocks of one packed 128-row tile
+                        tma_load_4d_hint(smem_a + stage * C::kBytesA, &tmap_a, &full_bar[stage], 0, 0, kb * KP, tm, pol_w);
                     else
                         tma_load_2d_hint(smem_a + stage * C::kBytesA, &tmap_a, &full_bar[stage], kb * BK, tm * BM, pol_w);
                 } else {
@@ -248,7 +253,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             };
             auto load_x = [&](int stage, int kb, int tm, int tn) {
-                if (p.swap)
+                if (p.swap && KP == 2)  // 3-D view (64 cols, tokens, k-block): box [2][BN][64]
+                    tma_load_3d(smem_b + stage * C::kBytesB, &tmap_b, &full_bar[stage], 0, tn * BN, kb * KP);
+                else if (p.swap)
                     tma_load_2d_hint(smem_b + stage * C::kBytesB, &tmap_b, &full_bar[stage], kb * BK, tn * BN, pol_x);
                 else
                     tma_load_2d_hint(smem_a + stage * C::kBytesA, &tmap_a, &full_bar[stage], kb * BK, tm * BM, pol_x);
@@ -309,11 +316,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t a_addr = smem_u32(smem_a + stage * C::kBytesA);
                     const uint32_t b_addr = smem_u32(smem_b + stage * C::kBytesB);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        const uint64_t ad = make_sw128_desc(a_addr + k * 32, 16, 1024);
-                        const uint64_t bd = make_sw128_desc(b_addr + k * 32, 16, 1024);
-                        umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-                    }
+                    for (int kk = 0; kk < KP; ++kk)
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k) {
+                            const uint64_t ad = make_sw128_desc(a_addr + kk * (BM * 128) + k * 32, 16, 1024);
+                            const uint64_t bd = make_sw128_desc(b_addr + kk * (BN * 128) + k * 32, 16, 1024);
+                            umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0 || k > 0) ? 1u : 0u);
+                        }
                     umma_commit(&empty_bar[stage]);
                 }
                 __syncwarp();
@@ -710,12 +719,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // Occupancy of S-CTA clusters of this kernel (cached per configuration).
-template <int BN>
+template <int BN, int KP>
 cudaError_t set_smem_attr();
 
-template <int BN>
+template <int BN, int KP = 1>
 int max_active_clusters(int S, cudaStream_t stream) {
-    if (set_smem_attr<BN>() != cudaSuccess) return 0;
+    if (set_smem_attr<BN, KP>() != cudaSuccess) return 0;
     static std::mutex mu;
     static std::map<std::pair<int, cudaStream_t>, int> cache;
     std::lock_guard<std::mutex> lock(mu);
@@ -724,7 +733,7 @@ int max_active_clusters(int S, cudaStream_t stream) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(S * 64, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = GemmCfg<BN>::kSmemBytes;
+    cfg.dynamicSmemBytes = GemmCfg<BN, KP>::kSmemBytes;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -734,7 +743,7 @@ int max_active_clusters(int S, cudaStream_t stream) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, gemm_tn_kernel<BN>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_tn_kernel<BN, KP>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         n = 0;
     }
@@ -742,21 +751,21 @@ int max_active_clusters(int S, cudaStream_t stream) {
     return n;
 }
 
-template <int BN>
+template <int BN, int KP>
 cudaError_t set_smem_attr() {
     static bool attr_set = false;  // per-process; harmless race (idempotent)
     if (attr_set) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         GemmCfg<BN>::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<BN, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         GemmCfg<BN, KP>::kSmemBytes);
     if (e == cudaSuccess) attr_set = true;
     return e;
 }
 
-template <int BN>
+template <int BN, int KP = 1>
 cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                       int num_sms, cudaStream_t stream, bool pdl) {
-    using C = GemmCfg<BN>;
-    cudaError_t e = set_smem_attr<BN>();
+    using C = GemmCfg<BN, KP>;
+    cudaError_t e = set_smem_attr<BN, KP>();
     if (e != cudaSuccess) return e;
     const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
     const bool staged = p.swap && (p.splits > 1 || p.epi == EPI_QKV);
@@ -783,7 +792,7 @@ cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const GemmPa
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, gemm_tn_kernel<BN>, ta, tb, p);
+    return cudaLaunchKernelEx(&cfg, gemm_tn_kernel<BN, KP>, ta, tb, p);
 }
 
 }  // namespace
@@ -795,17 +804,20 @@ int gemm_pick_bn(int n) {
     return 256;
 }
 
-int gemm_cluster_splits(int tiles, int k_blocks, int bn, int num_sms, cudaStream_t stream, int force) {
+int gemm_cluster_splits(int tiles, int k_blocks, int bn, int num_sms, cudaStream_t stream, int force, int kp) {
+    // k_blocks: pipeline k-units of kp 64-wide blocks
     auto fits = [&](int S) {
         if (S < 2) return true;
         const int kbps = (k_blocks + S - 1) / S;
         if ((S - 1) * kbps >= k_blocks) return false;  // an empty split
         int act = 0;
-        switch (bn) {
-        case 32: act = max_active_clusters<32>(S, stream); break;
-        case 64: act = max_active_clusters<64>(S, stream); break;
-        case 128: act = max_active_clusters<128>(S, stream); break;
-        default: act = max_active_clusters<256>(S, stream); break;
+        switch (bn * 4 + kp) {
+        case 32 * 4 + 1: act = max_active_clusters<32, 1>(S, stream); break;
+        case 32 * 4 + 2: act = max_active_clusters<32, 2>(S, stream); break;
+        case 64 * 4 + 1: act = max_active_clusters<64, 1>(S, stream); break;
+        case 64 * 4 + 2: act = max_active_clusters<64, 2>(S, stream); break;
+        case 128 * 4 + 1: act = max_active_clusters<128, 1>(S, stream); break;
+        default: act = max_active_clusters<256, 1>(S, stream); break;
         }
         return act >= tiles && tiles * S <= num_sms;
     };
@@ -821,19 +833,22 @@ int gemm_cluster_splits(int tiles, int k_blocks, int bn, int num_sms, cudaStream
 }
 
 cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int bn,
-                        int num_sms, cudaStream_t stream, bool pdl) {
-    const int k_blocks = (p.K + BK - 1) / BK;
+                        int num_sms, cudaStream_t stream, bool pdl, int kp) {
+    if (kp != 1 && !(kp == 2 && p.swap && bn <= 64)) return cudaErrorInvalidValue;
+    const int k_units = ((p.K + BK - 1) / BK + kp - 1) / kp;
     if (!p.swap || p.splits <= 1) {
         p.splits = 1;
-        p.kb_per_split = k_blocks;
+        p.kb_per_split = k_units;
     } else {
-        p.kb_per_split = (k_blocks + p.splits - 1) / p.splits;
+        p.kb_per_split = (k_units + p.splits - 1) / p.splits;
     }
-    switch (bn) {
-    case 32: return launch_bn<32>(ta, tb, p, num_sms, stream, pdl);
-    case 64: return launch_bn<64>(ta, tb, p, num_sms, stream, pdl);
-    case 128: return launch_bn<128>(ta, tb, p, num_sms, stream, pdl);
-    case 256: return launch_bn<256>(ta, tb, p, num_sms, stream, pdl);
+    switch (bn * 4 + kp) {
+    case 32 * 4 + 1: return launch_bn<32, 1>(ta, tb, p, num_sms, stream, pdl);
+    case 32 * 4 + 2: return launch_bn<32, 2>(ta, tb, p, num_sms, stream, pdl);
+    case 64 * 4 + 1: return launch_bn<64, 1>(ta, tb, p, num_sms, stream, pdl);
+    case 64 * 4 + 2: return launch_bn<64, 2>(ta, tb, p, num_sms, stream, pdl);
+    case 128 * 4 + 1: return launch_bn<128, 1>(ta, tb, p, num_sms, stream, pdl);
+    case 256 * 4 + 1: return launch_bn<256, 1>(ta, tb, p, num_sms, stream, pdl);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -78,15 +78,23 @@ int gemm_pick_bn(int n);
 int gemm_smem_bytes(int bn);
 // Cluster split-K factor for a swap-path GEMM of `tiles` weight tiles: the largest S <= 8
 // whose tiles*S clusters fit co-resident on num_sms SMs with no empty K split (1 = none).
+// k_blocks counts pipeline k-units of kp 64-wide blocks.
 int gemm_cluster_splits(int tiles, int k_blocks, int bn, int num_sms, cudaStream_t stream,
-                        int force = 0);
+                        int force = 0, int kp = 1);
 // pdl: launch with programmatic stream serialization (overlaps the previous kernel's tail).
+// kp = 2 (swap path, bn <= 64): two k-blocks per stage; ta must then be a packed weight map
+// with a 2-k-block box (make_tmap_packed(..., box_kb = 2)) and tb an activation k-pair map
+// (make_tmap_act_kpair).
 cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int bn,
-                        int num_sms, cudaStream_t stream, bool pdl = false);
+                        int num_sms, cudaStream_t stream, bool pdl = false, int kp = 1);
 
 // 4-D map over a tile-packed weight [N/128][K/64][128][64]: box = box_tiles x [128][64], so
 // every TMA box is box_tiles contiguous 16 KiB chunks.
-bool make_tmap_packed(CUtensorMap* out, const void* base, int rows_padded, int cols, int box_tiles);
+bool make_tmap_packed(CUtensorMap* out, const void* base, int rows_padded, int cols, int box_tiles,
+                      int box_kb = 1);
+// 3-D view (64 cols, rows, k-block) of a row-major bf16 [rows][cols] activation, box
+// [2 k-blocks][box_rows][64], SWIZZLE_128B: both k-blocks of a decode GEMM stage in one request.
+bool make_tmap_act_kpair(CUtensorMap* out, const void* base, int rows, int cols, int box_rows);
 // 3-D bf16 map over [d2][d1][d0] (d0 contiguous), box = [b2][b1][64], SWIZZLE_128B.
 bool make_tmap_bf16_3d(CUtensorMap* out, const void* base, int d0, int d1, int d2, int b1, int b2);
 // 2-D bf16 tensor map, row-major [rows][cols], box = [box_rows][64 cols], SWIZZLE_128B.

@@ -175,7 +175,8 @@ static void* dmalloc(size_t bytes, std::vector<void*>& track) {
 // instead of 128 strided 128-byte pieces.
 static void weight_maps(Weight& w) {
     if (!make_tmap_packed(&w.map_b256, w.ptr, w.rows_pad, w.cols, 2) ||
-        !make_tmap_packed(&w.map_a128, w.ptr, w.rows_pad, w.cols, 1))
+        !make_tmap_packed(&w.map_a128, w.ptr, w.rows_pad, w.cols, 1) ||
+        !make_tmap_packed(&w.map_a128k2, w.ptr, w.rows_pad, w.cols, 1, 2))
         fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for a weight");
 }
 
@@ -285,7 +286,7 @@ struct asb_lane {
     unsigned long long* mk_dbg = nullptr;  // ASB_MK_TIMELINE=1: per-CTA phase start stamps
     unsigned long long* attn_dbg = nullptr;  // ASB_ATTN_TIMELINE=1: decode-attention CTA stamps
     bool mega = std::getenv("ASB_MEGA") != nullptr && std::atoi(std::getenv("ASB_MEGA")) != 0;  // opt-in
-    CUtensorMap map_x[5];
+    CUtensorMap map_x[7];
     bool pdl = std::getenv("ASB_NO_PDL") == nullptr;  // programmatic dependent launch
     unsigned long long* dbg_times = nullptr;  // ASB_GEMM_TIMELINE: per-CTA stamps of the last GEMM
     size_t ppart_rows = 0;
@@ -296,7 +297,7 @@ struct asb_lane {
     size_t meta_ints = 0;
     std::vector<void*> allocs;
     // tensor maps of GEMM inputs: [0] box 128 (normal A), [1..4] box 32/64/128/256 (swap B)
-    CUtensorMap map_h[5], map_attn[5], map_act[5], map_hl[5], map_q;
+    CUtensorMap map_h[7], map_attn[7], map_act[7], map_hl[7], map_q;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool launched = false;
     int last_logit_rows = 0;
@@ -370,11 +371,16 @@ struct asb_lane {
 
 namespace {
 
+// [0] box 128 rows (normal-path A), [1..4] box 32/64/128/256 (swap-path B), [5..6] k-pair
+// boxes of 32/64 rows (swap-path B with two k-blocks per stage)
+constexpr int kActMaps = 7;
 void act_maps(CUtensorMap* maps, const void* base, int rows, int cols) {
     const int boxes[5] = {128, 32, 64, 128, 256};
     for (int i = 0; i < 5; ++i)
         if (!make_tmap_bf16(&maps[i], base, rows, cols, cols, boxes[i]))
             fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for an activation");
+    if (!make_tmap_act_kpair(&maps[5], base, rows, cols, 32) || !make_tmap_act_kpair(&maps[6], base, rows, cols, 64))
+        fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for an activation (k-pair)");
 }
 
 int swap_map_index(int bn) { return bn == 32 ? 1 : bn == 64 ? 2 : bn == 128 ? 3 : 4; }
@@ -471,10 +477,14 @@ void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
         p.M = w.rows;
         p.N = T;
         const int tiles = (w.rows + 127) / 128;
-        const int kb = (w.cols + 63) / 64;
+        // BN <= 64: two k-blocks per pipeline stage (32 KiB weight requests; ASB_GEMM_KP=1 off)
+        static const bool kp1 = std::getenv("ASB_GEMM_KP") && std::atoi(std::getenv("ASB_GEMM_KP")) == 1;
+        const int kp = (bn <= 64 && !kp1) ? 2 : 1;
+        const int kb = ((w.cols + 63) / 64 + kp - 1) / kp;
         // fewer weight tiles than SMs: split K over an S-CTA cluster per tile (DSMEM reduce)
-        p.splits = gemm_cluster_splits(tiles, kb, bn, num_sms, L->stream, force_splits);
-        e = gemm_launch(w.map_a128, xmaps[swap_map_index(bn)], p, bn, num_sms, L->stream, pdl);
+        p.splits = gemm_cluster_splits(tiles, kb, bn, num_sms, L->stream, force_splits, kp);
+        e = kp == 2 ? gemm_launch(w.map_a128k2, xmaps[bn == 32 ? 5 : 6], p, bn, num_sms, L->stream, pdl, 2)
+                    : gemm_launch(w.map_a128, xmaps[swap_map_index(bn)], p, bn, num_sms, L->stream, pdl);
     } else {
         p.swap = 0;
         p.b_packed = 1;
@@ -1327,7 +1337,7 @@ asb_status asb_debug_gemm_bench(const void* x, const void* w, void* out, int tok
             cuda_check(pack_weights(static_cast<const __nv_bfloat16*>(w), W.ptr, n_out, k, nullptr), "pack");
             weight_maps(W);
         }
-        CUtensorMap xm[5];
+        CUtensorMap xm[7];
         act_maps(xm, x, tokens, k);
         asb_model fake;
         int dev = 0;
@@ -1382,7 +1392,7 @@ asb_status asb_debug_gemm(const void* x, const void* w, const void* bias, const 
         cuda_check(pack_weights(static_cast<const __nv_bfloat16*>(w), W.ptr, n_out, k,
                                 static_cast<cudaStream_t>(stream)), "pack");
         weight_maps(W);
-        CUtensorMap xm[5];
+        CUtensorMap xm[7];
         act_maps(xm, x, tokens, k);
         asb_lane tmp;  // only stream and sms are used by linear()
         asb_model fake;

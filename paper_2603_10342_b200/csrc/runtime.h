@@ -22,6 +22,7 @@ struct Weight {
     int rows = 0, rows_pad = 0, cols = 0;
     CUtensorMap map_b256;  // B operand of the normal path (box 256 rows)
     CUtensorMap map_a128;  // A operand of the swap path / B with BN=128 (box 128 rows)
+    CUtensorMap map_a128k2;  // swap path, two k-blocks per stage (box [2][128][64], 32 KiB)
 };
 
 uint64_t substream_state(uint64_t seed, const std::string& name);

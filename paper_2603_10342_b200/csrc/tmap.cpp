@@ -60,16 +60,30 @@ bool make_tmap_bf16_3d(CUtensorMap* out, const void* base, int d0, int d1, int d
     return r == CUDA_SUCCESS;
 }
 
-bool make_tmap_packed(CUtensorMap* out, const void* base, int rows_padded, int cols, int box_tiles) {
+bool make_tmap_packed(CUtensorMap* out, const void* base, int rows_padded, int cols, int box_tiles,
+                      int box_kb) {
     EncodeFn enc = get_encode();
     if (!enc) return false;
     const int kb = cols / 64, nt = rows_padded / 128;
     cuuint64_t dims[4] = {64, 128, static_cast<cuuint64_t>(kb), static_cast<cuuint64_t>(nt)};
     cuuint64_t strides[3] = {128, 128 * 128, static_cast<cuuint64_t>(kb) * 128 * 128};
-    cuuint32_t box[4] = {64, 128, 1, static_cast<cuuint32_t>(box_tiles)};
+    cuuint32_t box[4] = {64, 128, static_cast<cuuint32_t>(box_kb), static_cast<cuuint32_t>(box_tiles)};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool make_tmap_act_kpair(CUtensorMap* out, const void* base, int rows, int cols, int box_rows) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>((cols + 63) / 64)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 2, 128};
+    cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 2};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
