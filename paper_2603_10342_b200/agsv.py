@@ -161,6 +161,18 @@ class Trace:
         st = self.api.L.agsv_trace_replay_check(self.h, C.byref(out))
         return st, json.loads(self.api._take(out))
 
+    def verify(self, params: dict | None = None) -> tuple[str, int, int, int]:
+        """agsv_verify_trace: (report JSON text, violations, vacuous, assumptions_met)."""
+        rep = C.c_void_p()
+        self.api._check(self.api.L.agsv_verify_trace(self.h, json.dumps(params or {}).encode(), C.byref(rep)))
+        try:
+            out = C.c_void_p()
+            self.api._check(self.api.L.agsv_report_json(rep, C.byref(out)))
+            return (self.api._take(out), self.api.L.agsv_report_violation_count(rep),
+                    self.api.L.agsv_report_vacuous_count(rep), self.api.L.agsv_report_assumptions_met(rep))
+        finally:
+            self.api.L.agsv_report_free(rep)
+
     @property
     def workload_hash(self) -> int:
         return self.api.L.agsv_trace_workload_hash(self.h)

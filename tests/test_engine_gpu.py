@@ -130,3 +130,20 @@ def test_wall_clock_run(built_lib, policy):
     _oracle_check(recs)
     if policy == "agentserve":
         assert foot["device"]["green_contexts"] in (True, False)
+
+
+def test_verify_on_wall_clock_trace(built_lib, tmp_path):
+    """Competitive-ratio verification on a REAL B200 trace: the interval
+    ledger holds the prefill tokens the kernels processed per Δt; our agsv_verify_trace and the
+    unmodified reference verifier read the same trace and must report the same thing."""
+    cfg = json.loads(json.dumps(MULTI))
+    cfg["slo"] = {"tau_tpot_ms": 20.0, "tau_ttft_ms": 2000.0}
+    cfg["controller"] = {"delta_t_ms": 50.0}
+    t = Agsv().run(_with_backend(cfg, "wall"))
+    got = t.verify()
+    rep = json.loads(got[0])
+    assert rep["schema"] == "agentsim-verify-v1"
+    assert rep["checked"] + rep["vacuous"] == len(rep["intervals"]) > 0
+    path = tmp_path / "wall.jsonl"
+    t.save(path)
+    assert ref_api().load_trace(path).verify() == got

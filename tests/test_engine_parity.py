@@ -152,3 +152,44 @@ def test_profile_documents_identical(apis):
     mine, ref = apis
     for shape in (None, {"decode_knee": 0.9, "cold_knee": 0.3}, {"total_sms": 144, "granularity": 16}):
         assert mine.profile_generate(shape) == ref.profile_generate(shape)
+
+
+VERIFY_CFGS = [
+    {"workload": {"paradigm": "react", "concurrency": 9}, "policy": "agentserve", "seed": 16},
+    {"workload": {"paradigm": "plan_and_execute", "concurrency": 4}, "policy": "agentserve", "seed": 11},
+    {"workload": {"paradigm": "react", "concurrency": 32, "model": "qwen2.5-3b"}, "policy": "agentserve", "seed": 13},
+    {"workload": {"concurrency": 4, "tool_delay": {"kind": "uniform", "min_ms": 10, "max_ms": 400}},
+     "controller": {"theta_low_ms": 5.0, "theta_high_ms": 30.0, "delta_t_ms": 100.0},
+     "policy": "agentserve", "seed": 11},
+    {"workload": {"paradigm": "react", "concurrency": 6}, "policy": "static_partition",
+     "static_decode_slots": 3, "seed": 5},
+]
+
+
+@pytest.mark.parametrize("cfg", VERIFY_CFGS, ids=lambda c: f"{c['policy']}-{c['seed']}")
+@pytest.mark.parametrize("params", [None, {"delta_sms": 24.0}, {"eps_bar": 0.001}, {"delta_sms": 0.0, "eps_bar": 0.0}])
+def test_verify_report_identical(apis, tmp, cfg, params):
+    """agsv_verify_trace (competitive-ratio bound check, analysis.cpp:160-242) produces the
+    reference's report byte for byte, and the reference verifies our trace to the same report."""
+    mine, ref = apis
+    tm, tr = mine.run(cfg), ref.run(cfg)
+    got, want = tm.verify(params), tr.verify(params)
+    assert got == want
+    path = f"{tmp}/verify_{cfg['policy']}_{cfg['seed']}.jsonl"
+    tm.save(path)
+    assert ref.load_trace(path).verify(params) == want
+    rep = json.loads(got[0])
+    assert rep["schema"] == "agentsim-verify-v1"
+    assert rep["checked"] + rep["vacuous"] == len(rep["intervals"])
+
+
+@pytest.mark.parametrize("params", ["{not json", json.dumps({"eps_bar": 1.5}), json.dumps({"delta_sms": -1.0})])
+def test_verify_error_statuses_match(apis, params):
+    import ctypes
+    mine, ref = apis
+    sts = []
+    for api in (mine, ref):
+        t = api.run(VERIFY_CFGS[0])
+        rep = ctypes.c_void_p()
+        sts.append(api.L.agsv_verify_trace(t.h, params.encode(), ctypes.byref(rep)))
+    assert sts[0] == sts[1] and sts[0] != 0
