@@ -109,7 +109,8 @@ def test_lockstep_matches_reference_and_oracle(built_lib, cfg):
     _oracle_check(dev)
 
 
-@pytest.mark.parametrize("policy", ["agentserve", "mixed_fcfs", "static_partition", "chunked_prefill"])
+@pytest.mark.parametrize("policy", ["agentserve", "mixed_fcfs", "static_partition", "chunked_prefill",
+                                    "agentserve_no_slots"])
 def test_wall_clock_run(built_lib, policy):
     cfg = json.loads(json.dumps(MULTI))
     cfg["policy"] = policy
