@@ -1,5 +1,6 @@
 #include "devexec.h"
 
+#include <cstdio>
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -177,9 +178,23 @@ void DeviceExec::step_launch(const std::vector<Row>& rows, int64_t chunk_s, cons
     }
     step_logit_rows_ = static_cast<int>(rows.size()) + (chunk_s >= 0 && chunk_n > 0 && chunk_logits ? 1 : 0);
     ok(asb_forward(dlane_, kv_, segs.data(), static_cast<int>(segs.size()), toks.data()), "decode step");
+    step_t0_ = now_ms();
+    static const bool trace_launch = std::getenv("AGENTSERVE_TRACE_LAUNCHES") != nullptr;
+    if (trace_launch)
+        std::fprintf(stderr, "[%9.3f] step rows=%zu chunk=%d sms=%d\n", step_t0_, rows.size(), chunk_n, dsms_);
+    step_what_ = "decode step (" + std::to_string(rows.size()) + " rows + chunk " + std::to_string(chunk_n) +
+                 " on " + std::to_string(dsms_) + " SMs)";
 }
 
-bool DeviceExec::step_ready() const { return asb_lane_query(dlane_) == 1; }
+// A launch that has not completed after kLaunchTimeoutMs is a device fault: fail the run with
+// the launch named instead of spinning forever.
+static constexpr double kLaunchTimeoutMs = 10000.0;
+
+bool DeviceExec::step_ready() const {
+    if (asb_lane_query(dlane_) == 1) return true;
+    if (now_ms() - step_t0_ > kLaunchTimeoutMs) raise(Err::Protocol, step_what_ + " did not complete in 10 s");
+    return false;
+}
 
 std::vector<int32_t> DeviceExec::step_collect(float* dev_ms) {
     std::vector<int32_t> ids(static_cast<size_t>(std::max(step_logit_rows_, 1)));
@@ -193,9 +208,19 @@ void DeviceExec::prefill_launch(uint32_t s, const int32_t* toks, int n, bool wan
     asb_segment g{s, n, want ? 1 : 0};
     prefill_want_ = want;
     ok(asb_forward(plane_, kv_, &g, 1, toks), "prefill unit");
+    pre_t0_ = now_ms();
+    static const bool trace_launch = std::getenv("AGENTSERVE_TRACE_LAUNCHES") != nullptr;
+    if (trace_launch)
+        std::fprintf(stderr, "[%9.3f] prefill s=%u n=%d len=%d sms=%d\n", pre_t0_, s, n, asb_kv_length(kv_, s), psms_);
+    pre_what_ = "prefill unit (" + std::to_string(n) + " tokens of session " + std::to_string(s) + " at length " +
+                std::to_string(asb_kv_length(kv_, s)) + " on " + std::to_string(psms_) + " SMs)";
 }
 
-bool DeviceExec::prefill_ready() const { return asb_lane_query(plane_) == 1; }
+bool DeviceExec::prefill_ready() const {
+    if (asb_lane_query(plane_) == 1) return true;
+    if (now_ms() - pre_t0_ > kLaunchTimeoutMs) raise(Err::Protocol, pre_what_ + " did not complete in 10 s");
+    return false;
+}
 
 int32_t DeviceExec::prefill_collect(float* dev_ms) {
     int32_t id = -1;

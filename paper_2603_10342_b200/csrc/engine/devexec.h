@@ -89,6 +89,8 @@ private:
     std::vector<std::vector<int32_t>> cold_;
     std::vector<std::vector<std::vector<int32_t>>> resume_;
     std::chrono::steady_clock::time_point t0_;
+    double step_t0_ = 0.0, pre_t0_ = 0.0;  // launch times (watchdog)
+    std::string step_what_, pre_what_;
     nlohmann::json info_;
 };
 

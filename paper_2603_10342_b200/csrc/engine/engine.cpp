@@ -491,7 +491,14 @@ private:
 
     void start_prefill_unit() {
         if (span_ || qp_.empty()) return;
-        if (!split_.shared && split_.pslots == 0) return;  // partition owns no SMs right now
+        if (!split_.shared && split_.pslots == 0) {
+            // The partition owns no SMs right now.  Virtual clocks wait (reference semantics).
+            // On real kernels a one-row step at R = S/g stays between the controller's
+            // thresholds, so R never shrinks and Q_P would starve for ever (livelock seen at
+            // C3, 32 agents): run the unit on the stream the lane is bound to (the full device
+            // at that level), between decode steps.
+            if (clock_ != Clock::Wall || stepping_) return;
+        }
         Job& j = qp_.front();
         const int sms = psms();
         const double rate = j.kind == ReqKind::Cold ? prof_.mu_c(sms) : prof_.mu_r(sms);

@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 continue;
             }
 #pragma unroll 1
-            for (int c = 0; c < BN && (!p.swap || c < p.tokens); c += 32) {
+            for (int c = 0; c < BN && (!p.swap || c < p.tokens) && !p.dbg_no_epi; c += 32) {
                 uint32_t r[32];
                 tmem_ld32(t_row + c, r);
                 tmem_ld_wait();

@@ -45,6 +45,7 @@ struct GemmParams {
     unsigned long long* amax;  // swap + EPI_F32 only, optional: per-token argmax_key accumulator
                                // (atomicMax; zero on entry) -- the LM head's greedy sample
     unsigned long long* dbg_times;  // optional per-CTA timeline [grid][8] (globaltimer ns)
+    int dbg_no_epi;                 // timing ablation: epilogue drains TMEM but stores nothing
 };
 
 // Small-batch decode linear (dgemv.cu): T <= dgemv_max_tokens() rows of X against a

@@ -21,6 +21,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", choices=["c2", "c3"], default="c2")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--out", default=None)
+ap.add_argument("--policies", nargs="*", default=None, help="subset, e.g. agentserve mixed_fcfs static_partition:3")
+ap.add_argument("--horizon-ms", type=float, default=None)
 a = ap.parse_args()
 api = Agsv()
 
@@ -40,12 +42,17 @@ else:  # C3: Llama-3.2-3B-shaped, 32 ReAct agents, shaped profil
 slots = json.loads(json.dumps(base["profile"]["inline"]))["total_sms"] // json.loads(json.dumps(base["profile"]["inline"]))["granularity"]
 runs = [("agentserve", None), ("mixed_fcfs", None), ("chunked_prefill", None), ("agentserve_no_slots", None)]
 runs += [("static_partition", k) for k in range(1, slots)]
+if a.policies:
+    want = [(x.split(":")[0], int(x.split(":")[1]) if ":" in x else None) for x in a.policies]
+    runs = [r for r in runs if r in want]
 rows = []
 for pol, k in runs:
     cfg = json.loads(json.dumps(base))
     cfg["policy"] = pol
     if k is not None:
         cfg["static_decode_slots"] = k
+    if a.horizon_ms:
+        cfg["horizon_ms"] = a.horizon_ms
     ms = []
     for _ in range(a.reps):
         t = api.run(cfg)
