@@ -241,24 +241,34 @@ def _pct(xs: list[float], p: float) -> float | None:
     return s[min(k, len(s)) - 1]
 
 
+def device_index() -> tuple[int, int]:
+    """(CUDA ordinal in this process, physical GPU index for nvidia-smi) of this rank: one rank
+    per GPU.  A launcher that pins one device per process through CUDA_VISIBLE_DEVICES leaves
+    ordinal 0; otherwise the rank's LOCAL_RANK selects the device."""
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cvd = [x.strip() for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip()]
+    if len(cvd) == 1:
+        return 0, int(cvd[0]) if cvd[0].isdigit() else local
+    if cvd and local < len(cvd) and cvd[local].isdigit():
+        return local, int(cvd[local])
+    return local, local
+
+
 def run_mine(args) -> None:
     n_gpus, rank, dist = _dist()
-    if n_gpus > 1 and dist.get_backend() == "nccl":
-        local = int(os.environ.get("LOCAL_RANK", rank))
-        os.environ.setdefault("CUDA_VISIBLE_DEVICES", str(local))
     import torch
+    dev_idx, phys_idx = device_index()
     if args.virtual:
         clock = "virtual"
     else:
         clock = "wall"
-        local = int(os.environ.get("LOCAL_RANK", 0))
-        torch.cuda.set_device(local)
+        torch.cuda.set_device(dev_idx)
     from paper_2603_10342_b200.agsv import Agsv
     api = Agsv()
     prof_doc, prof_src = profile_doc(api)
     cfg = workload_config(n_gpus, rank, clock, args.policy, prof_doc)
     if clock == "wall":
-        cfg["backend"]["device"] = int(os.environ.get("LOCAL_RANK", 0)) if os.environ.get("CUDA_VISIBLE_DEVICES") is None else 0
+        cfg["backend"]["device"] = dev_idx
     td = tempfile.mkdtemp()
 
     def episode(c=cfg):
@@ -275,7 +285,7 @@ def run_mine(args) -> None:
         dist.barrier()
     if clock == "wall":
         torch.cuda.synchronize()
-        sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
+        sampler = ClockSampler(phys_idx)
         sampler.start()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()

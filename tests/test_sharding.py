@@ -10,6 +10,8 @@ import sys
 import tempfile
 from pathlib import Path
 
+import pytest
+
 from paper_2603_10342_b200.agsv import Agsv
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -60,3 +62,20 @@ def test_bench_torchrun_gloo_two_ranks(built_lib):
     assert d["n_gpus"] == 2 and d["scaling"] == "weak"
     assert d["latency_ms"]["sessions"] == 16  # 8 agents per rank, both ranks counted
     assert d["value"] > 0
+
+
+@pytest.mark.parametrize("env,want", [
+    ({"LOCAL_RANK": "3"}, (3, 3)),                                  # torchrun, all GPUs visible
+    ({"LOCAL_RANK": "3", "CUDA_VISIBLE_DEVICES": "5"}, (0, 5)),     # launcher pins one GPU per rank
+    ({"LOCAL_RANK": "1", "CUDA_VISIBLE_DEVICES": "4,6"}, (1, 6)),   # a visible subset
+    ({}, (0, 0)),
+])
+def test_bench_device_index(monkeypatch, env, want):
+    """One rank per GPU: the CUDA ordinal the rank binds (and the physical index nvidia-smi
+    samples) for the launch patterns the driver may use."""
+    import bench
+    for k in ("LOCAL_RANK", "CUDA_VISIBLE_DEVICES"):
+        monkeypatch.delenv(k, raising=False)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    assert bench.device_index() == want
