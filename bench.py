@@ -384,14 +384,21 @@ def run_mine(args) -> None:
         hbm = dom["unit"] == "bytes"
         achieved = dom["units"] / (dom["ms"] / 1000.0) / (1e9 if hbm else 1e12)
         peak = peaks["hbm"] if hbm else peaks["bf16_sust"]
-        traffic = None
+        # DRAM bytes per launch of this category from an ncu capture of C2-shaped decode steps
+        # (scripts/ncu_traffic.py), and their ratio to the algorithmic bytes of the same launches
+        traffic, traffic_ratio = None, None
         tf = ROOT / "profiles" / "ncu_traffic.json"
         if tf.exists():
-            traffic = json.loads(tf.read_text()).get(dom_name)
+            tdoc = json.loads(tf.read_text())
+            traffic = tdoc.get(dom_name)
+            alg = tdoc.get(f"_algorithmic_{dom_name}_per_launch")
+            if traffic and alg:
+                traffic_ratio = round(traffic / alg, 4)
         line["roofline"] = {"kernel": dom_name, "bound": "hbm" if hbm else "tensor",
                             "achieved": round(achieved, 2), "peak": peak,
                             "unit": "GB/s" if hbm else "TFLOP/s", "frac": round(achieved / peak, 4),
-                            "traffic": traffic, "peak_source": peaks["src"],
+                            "traffic": round(traffic) if traffic else None,
+                            "traffic_over_algorithmic": traffic_ratio, "peak_source": peaks["src"],
                             "avg_launch_us": round(1000.0 * dom["ms"] / max(1, dom["launches"]), 2),
                             "share_of_device_time": round(dom["ms"] / sum(v["ms"] for v in kern.values()), 3),
                             "measured": "profiled replay of the timed episode (CUDA events per launch)"}
