@@ -403,10 +403,14 @@ struct XIn {
 bool use_dgemv(int T, const Weight& w, int num_sms) {
     static const bool off = std::getenv("ASB_NO_DGEMV") && std::atoi(std::getenv("ASB_NO_DGEMV")) != 0;
     const double bytes = 2.0 * double(w.rows) * w.cols;
-    // measured crossover (profiles/r1_gemm_bench_partitions.json): dgemv wins while each SM
-    // of the partition streams <= ~160 KB of the weight; beyond that the TMA-fed tcgen05
-    // kernel keeps more bytes in flight per SM
-    return !off && T <= (bytes / num_sms <= 160e3 ? 16 : 0);
+    // Measured crossover: in isolation dgemv wins while each SM of the partition streams
+    // <= ~160 KB of the weight (profiles/r1_gemm_bench_partitions.json), but inside a decode
+    // step on <= 32 SMs the all-tcgen05 chain is faster (1.71 vs 1.78 ms at 16 SMs, 1.31 vs
+    // 1.32 at 32): dgemv's two 8-warp CTAs fill an SM's registers, so the next PDL launch
+    // cannot become resident and prefetch its weights; from 64 SMs up dgemv wins (1.02 vs
+    // 1.10 ms at 64, 0.84 vs 0.97 at 148; scripts/step_launches.py --level=L, B=2).
+    const double per_sm = bytes / num_sms;
+    return !off && T <= 16 && num_sms > 32 && per_sm <= 160e3;
 }
 
 // Y[T][n_out] = X[T][k] . W^T with the path chosen by T (path 2 = dgemv, 1 = tcgen05
