@@ -85,11 +85,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
-__device__ __forceinline__ uint4 ldcg128(const void* p) {
-    uint4 v;
-    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-    return v;
-}
 __device__ __forceinline__ float bf16cg(const __nv_bfloat16* p) {
     const unsigned short u = __ldcg(reinterpret_cast<const unsigned short*>(p));
     return __uint_as_float(static_cast<uint32_t>(u) << 16);
@@ -145,32 +140,6 @@ __device__ __forceinline__ void wait_gen_cta(const unsigned* gen_s, unsigned tar
         __nanosleep(32);
         if (gtime() - t0 > kTimeoutNs) __trap();
     }
-}
-
-// RMSNorm statistics of one row through L2 (rows are rewritten by other SMs during the step,
-// so the L1 must not be used); same operation order as rms_inv_warp.
-__device__ __forceinline__ float rms_inv_warp_cg(const __nv_bfloat16* row, int d, float eps, int lane) {
-    float ss = 0.f;
-    const int n = d / 8;
-    for (int i0 = lane; i0 < n; i0 += 4 * 32) {  // 4 loads in flight per lane, then sum in order
-        uint4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (i0 + 32 * u < n) v[u] = ldcg128(row + 8 * (i0 + 32 * u));
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (i0 + 32 * u >= n) break;
-            const uint32_t a[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float lo = bf16_lo(a[e]), hi = bf16_hi(a[e]);
-                ss = __fadd_rn(ss, __fadd_rn(__fmul_rn(lo, lo), __fmul_rn(hi, hi)));
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
-    return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, static_cast<float>(d)), eps)));
 }
 
 struct Gemv {

@@ -306,6 +306,8 @@ __global__ void __launch_bounds__(WARPS * 32, (DgCfg<NT, WARPS>::kMinBlocks)) dg
         break;
     }
     }
+    // fused next pre-norm (decode steps): the last CTA normalises the updated residual rows
+    if (p.post.w && grid_last_arriver(p.post.counter)) post_norm_rows(p.post, p.out, p.ldo);
 }
 
 template <int NT, int WARPS>

@@ -61,7 +61,8 @@ __global__ void pack_weights_kernel(const __nv_bfloat16* __restrict__ src, __nv_
 // Embedding gather from the tile-packed table: a row is d/64 contiguous 128-byte chunks.
 __global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ emb,
                              __nv_bfloat16* __restrict__ x, int T, int d,
-                             unsigned long long* __restrict__ zero_keys, int n_keys) {
+                             unsigned long long* __restrict__ zero_keys, int n_keys,
+                             const __nv_bfloat16* __restrict__ norm_w, __nv_bfloat16* __restrict__ h, float eps) {
     pdl_trigger();
     pdl_wait();
     const int t = blockIdx.x;
@@ -75,6 +76,24 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat1
     for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
         const int chunk = i >> 3, piece = i & 7;
         dst[i] = *reinterpret_cast<const uint4*>(emb + packed_off(R, chunk * 64 + piece * 8, kb, d));
+    }
+    if (!norm_w) return;
+    // layer 0's pre-norm of this row, fused (rmsnorm_kernel's arithmetic, bit-identical)
+    __shared__ float inv_s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const float inv = rms_inv_warp(x + static_cast<size_t>(t) * d, d, eps, threadIdx.x);
+        if (threadIdx.x == 0) inv_s = inv;
+    }
+    __syncthreads();
+    const float inv = inv_s;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * d);
+    const uint4* wr = reinterpret_cast<const uint4*>(norm_w);
+    uint4* hr = reinterpret_cast<uint4*>(h + static_cast<size_t>(t) * d);
+    for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
+        const uint4 v = xr[i], g = wr[i];
+        hr[i] = make_uint4(rms_apply2(v.x, g.x, inv), rms_apply2(v.y, g.y, inv), rms_apply2(v.z, g.z, inv),
+                           rms_apply2(v.w, g.w, inv));
     }
 }
 
@@ -205,9 +224,11 @@ cudaError_t pack_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, int64_t r
 }
 
 cudaError_t embed(const int32_t* ids, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int d,
-                  cudaStream_t stream, unsigned long long* zero_keys, int n_keys) {
+                  cudaStream_t stream, unsigned long long* zero_keys, int n_keys, const __nv_bfloat16* norm_w,
+                  __nv_bfloat16* h, float eps) {
     if (T <= 0) return cudaSuccess;
-    return launch_k(embed_kernel, dim3(T), dim3(128), 0, stream, ids, emb, x, T, d, zero_keys, n_keys);
+    return launch_k(embed_kernel, dim3(T), dim3(128), 0, stream, ids, emb, x, T, d, zero_keys, n_keys, norm_w, h,
+                    eps);
 }
 
 cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows_idx, const __nv_bfloat16* w,

@@ -14,8 +14,10 @@ cudaError_t init_weights(__nv_bfloat16* dst, uint64_t state0, int64_t rows, int 
 cudaError_t pack_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, int64_t rows, int cols,
                          cudaStream_t stream);
 // zero_keys (optional): zeroed [n_keys] argmax-key accumulator of the LM head of this forward.
+// norm_w (optional): also h[t] = layer 0's pre-norm of the row (rmsnorm_kernel arithmetic).
 cudaError_t embed(const int32_t* ids, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int d,
-                  cudaStream_t stream, unsigned long long* zero_keys = nullptr, int n_keys = 0);
+                  cudaStream_t stream, unsigned long long* zero_keys = nullptr, int n_keys = 0,
+                  const __nv_bfloat16* norm_w = nullptr, __nv_bfloat16* h = nullptr, float eps = 0.f);
 // zero_keys (optional): zeroed [n_rows] argmax-key accumulator for the LM head that follows.
 cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows_idx, const __nv_bfloat16* w,
                     __nv_bfloat16* y, int n_rows, int d, float eps, cudaStream_t stream,

@@ -716,6 +716,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         tmem_dealloc<C::kTmemCols>(tmem_base);
     }
+    // fused next pre-norm (decode steps): the last CTA normalises the updated residual rows
+    if (p.post.w && grid_last_arriver(p.post.counter)) post_norm_rows(p.post, p.out, p.ldo);
 }
 
 // Occupancy of S-CTA clusters of this kernel (cached per configuration).

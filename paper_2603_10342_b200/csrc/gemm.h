@@ -27,6 +27,18 @@ struct RopeEpi {
     int hq, hkv, hd, layer, num_blocks;
 };
 
+// Fused "next pre-norm" of a residual-writing linear (EPI_RESID): the last CTA of the grid
+// normalises rows of the updated residual stream x into `out` (decode-sized batches only).
+struct PostNorm {
+    const __nv_bfloat16* w = nullptr;  // null: off
+    __nv_bfloat16* out = nullptr;      // [n_rows][d]
+    const int32_t* rows = nullptr;     // source row of output row r (null: r)
+    int n_rows = 0, d = 0;
+    float eps = 0.f;
+    int* counter = nullptr;            // zero-initialised grid arrival counter
+    unsigned long long* zero_keys = nullptr;
+};
+
 struct GemmParams {
     int M, N, K;          // kernel view: D[M][N] = A[M][K] . B[N][K]^T
     int tokens, n_out;    // logical view: Y[tokens][n_out]
@@ -45,6 +57,7 @@ struct GemmParams {
     unsigned long long* amax;  // swap + EPI_F32 only, optional: per-token argmax_key accumulator
                                // (atomicMax; zero on entry) -- the LM head's greedy sample
     unsigned long long* dbg_times;  // optional per-CTA timeline [grid][8] (globaltimer ns)
+    PostNorm post;                  // optional, EPI_RESID
     int dbg_no_epi;                 // timing ablation: epilogue drains TMEM but stores nothing
 };
 
@@ -70,6 +83,7 @@ struct DgemvParams {
     int ldr;
     RopeEpi rope;
     unsigned long long* amax;
+    PostNorm post;  // optional, EPI_RESID
     int rw;  // internal: row-warps per CTA
 };
 int dgemv_max_tokens();

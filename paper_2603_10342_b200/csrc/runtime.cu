@@ -273,6 +273,7 @@ struct asb_lane {
     __nv_bfloat16 *x, *h, *qkv, *q, *attn, *act, *hl;
     float *logits, *part_o, *part_ml, *ppart_o, *ppart_ml;
     int* dcnt = nullptr;  // decode-attention split arrival counters [rows][hkv] (self-resetting)
+    int* post_cnt = nullptr;  // grid arrival counter of the fused post-norm (self-resetting)
     // split merge inside the decode-attention kernel (last-arriving split) instead of a
     // combine launch; ASB_ATTN_COMBINE=1 selects the separate combine kernel
     bool attn_fused_merge = std::getenv("ASB_ATTN_COMBINE") == nullptr;
@@ -418,7 +419,7 @@ bool use_dgemv(int T, const Weight& w, int num_sms) {
 void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
             __nv_bfloat16* out, int ldo, const __nv_bfloat16* bias, const __nv_bfloat16* resid,
             float* out_f32, int force_path = -1, int force_splits = 0,
-            unsigned long long* amax = nullptr, const RopeEpi* rope = nullptr) {
+            unsigned long long* amax = nullptr, const RopeEpi* rope = nullptr, const PostNorm* post = nullptr) {
     const CUtensorMap* xmaps = xin.maps;
     if (force_path == 2 || (force_path < 0 && use_dgemv(T, w, L->n_sms()))) {
         DgemvParams d{};
@@ -441,6 +442,7 @@ void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
         d.ldr = ldo;
         if (rope) d.rope = *rope;
         d.amax = amax;
+        if (post) d.post = *post;
         L->n_launch += 1;
         const double units = 2.0 * (double(w.rows) * w.cols + double(T) * w.cols) +
                              double(T) * w.rows * (epi == EPI_F32 ? 4.0 : 2.0);
@@ -452,6 +454,7 @@ void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
     if (xin.norm_w || xin.rows) fail(ASB_ERR_INVALID_ARGUMENT, "fused norm / row gather needs the dgemv path");
     GemmParams p{};
     p.amax = amax;
+    if (post) p.post = *post;
     if (rope) p.rope = *rope;
     p.tokens = T;
     p.n_out = w.rows;
@@ -841,6 +844,8 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->part_ml = static_cast<float*>(
             dmalloc(size_t(dec_rows) * s.hq * L->max_splits * 2 * 4, L->allocs));
         L->dcnt = static_cast<int*>(dmalloc(size_t(dec_rows) * s.hkv * 4, L->allocs));
+        L->post_cnt = static_cast<int*>(dmalloc(64, L->allocs));
+        cuda_check(cudaMemset(L->post_cnt, 0, 64), "counters");
         cuda_check(cudaMemset(L->dcnt, 0, size_t(dec_rows) * s.hkv * 4), "counters");
         {
             const int rows = kMkMaxRows, G = s.hq / s.hkv;
@@ -1104,9 +1109,6 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
             }
         }
         if (!mega_done) {
-            cuda_check(embed(d_tok, m->embed.ptr, L->x, T, s.d, st,
-                             (n_logit > 0 && use_dgemv(n_logit, m->lm_head, L->n_sms())) ? L->d_out : nullptr, n_logit),
-                       "embed");
             // the fused QKV epilogue needs q/k/v regions aligned to the 128-row weight tiles
             // ASB_DEBUG_SKIP=attn,norm,...: timing ablation only (outputs are garbage)
             static const std::string skip_list = std::getenv("ASB_DEBUG_SKIP") ? std::getenv("ASB_DEBUG_SKIP") : "";
@@ -1119,13 +1121,31 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
             // LM-head launches apply the preceding RMSNorm themselves (no norm launch).
             const bool dg_qkv = use_dgemv(T, m->layers[0].qkv, L->n_sms()),
                        dg_gu = use_dgemv(T, m->layers[0].gate_up, L->n_sms());
+            const bool dg_lm = n_logit > 0 && use_dgemv(n_logit, m->lm_head, L->n_sms());
+            // Pre-norms of tcgen05 linears: layer 0's in the embedding kernel; on small decode
+            // batches the others in the residual GEMM before them (its last CTA normalises the
+            // updated rows, PostNorm) -- no separate norm launches.
+            // (one CTA normalises all T rows: worth a launch only while T x d is small -- at
+            // Llama-3.1-8B B=64 it costs 3.5 ms per step; Qwen2.5-0.5B B=2: -1%)
+            const bool post_ok = int64_t(T) * s.d <= 16 * 1024 && std::getenv("ASB_NO_POST_NORM") == nullptr;
+            const bool post_attn = !dg_qkv && post_ok, post_mlp = !dg_gu && post_ok;
+            const bool post_final = n_logit > 0 && !dg_lm && n_logit <= 256 && post_ok;
+            cuda_check(embed(d_tok, m->embed.ptr, L->x, T, s.d, st, dg_lm ? L->d_out : nullptr, n_logit,
+                             dg_qkv ? nullptr : m->layers[0].attn_norm, L->h, s.eps),
+                       "embed");
             // non-GEMM kernels of this forward (linear() counts its own launches): embed; per layer
             // the unfused norms, the unfused RoPE/append, decode attention (split merge fused) and
             // prefill attention (+ its split combine); final norm and argmax when not fused
-            L->n_launch += 1 + int64_t(s.layers) * ((dg_qkv ? 0 : 1) + (dg_gu ? 0 : 1) + (fuse_qkv ? 0 : 1) +
-                                                    (ditems.empty() ? 0 : 1) +
-                                                    (pitems.empty() ? 0 : (psplits > 1 ? 2 : 1)));
-            if (n_logit > 0 && !use_dgemv(n_logit, m->lm_head, L->n_sms())) L->n_launch += n_logit <= 256 ? 1 : 2;
+            L->n_launch += 1 + int64_t(s.layers - 1) * ((dg_qkv || post_attn) ? 0 : 1) +
+                           int64_t(s.layers) * ((dg_gu || post_mlp ? 0 : 1) + (fuse_qkv ? 0 : 1) +
+                                                (ditems.empty() ? 0 : 1) + (pitems.empty() ? 0 : (psplits > 1 ? 2 : 1)));
+            if (n_logit > 0 && !dg_lm) L->n_launch += (post_final ? 0 : 1) + (n_logit <= 256 ? 0 : 1);
+            PostNorm pn_attn{}, pn_mlp{}, pn_final{};
+            if (post_mlp || post_attn || post_final) {
+                pn_attn = PostNorm{nullptr, L->h, nullptr, T, s.d, s.eps, L->post_cnt, nullptr};
+                pn_mlp = pn_attn;
+                pn_final = PostNorm{m->final_norm, L->hl, d_lrows, n_logit, s.d, s.eps, L->post_cnt, L->d_out};
+            }
             const XIn x_attn{L->map_attn, L->attn, qd};
             const XIn x_act{L->map_act, L->act, s.ffn};
             for (int l = 0; l < s.layers; ++l) {
@@ -1135,7 +1155,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                                       : XIn{L->map_h, L->h, s.d};
                 const XIn xm = dg_gu ? XIn{nullptr, L->x, s.d, ly.mlp_norm, nullptr, s.eps}
                                      : XIn{L->map_h, L->h, s.d};
-                if (!dg_qkv && !skip("norm"))
+                if (!dg_qkv && l > 0 && !post_attn && !skip("norm"))
                     cuda_check(rmsnorm(L->x, nullptr, ly.attn_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
                 if (skip("qkv")) {
                 } else if (fuse_qkv) {
@@ -1164,24 +1184,39 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                                                      L->ppart_ml, as, st),
                                    "prefill attention");
                     });
-                if (!skip("o")) linear(L, x_attn, ly.o, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
-                if (!dg_gu && !skip("norm"))
+                pn_mlp.w = post_mlp ? ly.mlp_norm : nullptr;
+                if (!skip("o"))
+                    linear(L, x_attn, ly.o, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr, -1, 0, nullptr, nullptr,
+                           post_mlp ? &pn_mlp : nullptr);
+                if (!dg_gu && !post_mlp && !skip("norm"))
                     cuda_check(rmsnorm(L->x, nullptr, ly.mlp_norm, L->h, T, s.d, s.eps, st), "rmsnorm");
                 if (!skip("gate_up")) linear(L, xm, ly.gate_up, T, EPI_SILU, L->act, s.ffn, nullptr, nullptr, nullptr);
-                if (!skip("down")) linear(L, x_act, ly.down, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr);
+                // the residual GEMM closing the layer prepares the next pre-norm (next layer's
+                // attention norm, or the final norm of the LM-head rows after the last layer)
+                const bool last = l + 1 == s.layers;
+                const PostNorm* pn = nullptr;
+                if (!last && post_attn) {
+                    pn_attn.w = m->layers[l + 1].attn_norm;
+                    pn = &pn_attn;
+                } else if (last && post_final) {
+                    pn = &pn_final;
+                }
+                if (!skip("down"))
+                    linear(L, x_act, ly.down, T, EPI_RESID, L->x, s.d, nullptr, L->x, nullptr, -1, 0, nullptr, nullptr, pn);
             }
             if (n_logit > 0) {
                 // greedy sample fused into the LM head epilogue (<= 256 rows): the argmax keys are
                 // zeroed by the final norm (or, on the dgemv path, by the embedding kernel, and the
                 // LM head normalises and gathers its rows itself); the GEMM atomicMax-es into them
                 const bool fused_argmax = n_logit <= 256;
-                if (use_dgemv(n_logit, m->lm_head, L->n_sms())) {
+                if (dg_lm) {
                     XIn xl{nullptr, L->x, s.d, m->final_norm, d_lrows, s.eps};
                     linear(L, xl, m->lm_head, n_logit, EPI_F32, nullptr, s.vocab, nullptr, nullptr, L->logits, -1, 0,
                            L->d_out);
                 } else {
-                    cuda_check(rmsnorm(L->x, d_lrows, m->final_norm, L->hl, n_logit, s.d, s.eps, st,
-                                       fused_argmax ? L->d_out : nullptr), "final norm");
+                    if (!post_final)
+                        cuda_check(rmsnorm(L->x, d_lrows, m->final_norm, L->hl, n_logit, s.d, s.eps, st,
+                                           fused_argmax ? L->d_out : nullptr), "final norm");
                     linear(L, XIn{L->map_hl, L->hl, s.d}, m->lm_head, n_logit, EPI_F32, nullptr, s.vocab, nullptr,
                            nullptr, L->logits, -1, 0, fused_argmax ? L->d_out : nullptr);
                     if (!fused_argmax)
