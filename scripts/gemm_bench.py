@@ -32,6 +32,7 @@ ap.add_argument("--levels", type=int, nargs="+", default=[0],
                 help="green-context decode levels (SMs = level x 16 on B200); 0 = whole device")
 ap.add_argument("--models", nargs="+", default=list(SHAPES))
 ap.add_argument("--out", default=None)
+ap.add_argument("--prefill", action="store_true", help="normal (prefill) path 0 at the given token counts; TF/s")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 slots = Slots(0, levels=9, granularity=16)
@@ -50,13 +51,17 @@ for model in a.models:
                     stream, _ = slots.bind(lev)
                     sms = slots.sm_counts(lev)[0]
                 row = {"model": model, "linear": name, "T": T, "N": N, "K": K, "sms": sms or 148}
-                for path in ((1, 2) if T <= 32 else (1,)):
+                paths = (0,) if a.prefill else ((1, 2) if T <= 32 else (1,))
+                for path in paths:
                     us = C.c_float(0)
                     check(lib().asb_debug_gemm_bench(x.data_ptr(), w.data_ptr(), out.data_ptr(), T, N, K, epi, path,
                                                      50, sms, stream, C.byref(us)))
                     row[f"p{path}_us"] = round(us.value, 2)
                     row[f"p{path}_gbs"] = round(bytes_ / (us.value * 1e-6) / 1e9, 1)
-                row["p1_frac"] = round(row["p1_gbs"] / PEAK, 3)
+                    if a.prefill:
+                        row["tflops"] = round(2.0 * T * N * K / (us.value * 1e-6) / 1e12, 1)
+                if "p1_gbs" in row:
+                    row["p1_frac"] = round(row["p1_gbs"] / PEAK, 3)
                 if "p2_gbs" in row:
                     row["p2_frac"] = round(row["p2_gbs"] / PEAK, 3)
                 res.append(row)

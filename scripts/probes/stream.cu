@@ -4,11 +4,49 @@
 //   bulk : one thread issues cp.async.bulk of `chunk` bytes into a `stages`-deep mbarrier ring
 //   ldg  : 256 threads, `unroll` 16-byte ld.global.nc.L1::no_allocate per thread in flight
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2603_10342_b200/csrc scripts/probes/stream.cu -o /tmp/stream
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdint>
 #include "sm100.cuh"
+#include "gemm.h"
 using namespace asb;
+
+// 4-D tensor TMA over a tile-packed weight view [nt][kb][128][64] bf16 (box [kbox][128][64]),
+// the decode GEMM's weight stream, vs the same bytes by 1-D bulk copies
+__global__ void __launch_bounds__(64, 1) stream_tma4d(const __grid_constant__ CUtensorMap map, int nt, int kbs,
+                                                       int kbox, int stages, unsigned long long* sink) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    const int chunk = kbox * 16384;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)stages * chunk);
+    uint64_t* empty = full + stages;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        fence_barrier_init();
+        tma_prefetch_desc(&map);
+    }
+    __syncthreads();
+    const int t0 = (nt * blockIdx.x) / gridDim.x, t1 = (nt * (blockIdx.x + 1)) / gridDim.x;
+    const long long n = (long long)(t1 - t0) * (kbs / kbox);
+    if (threadIdx.x == 0) {
+        for (long long i = 0; i < n; ++i) {
+            const int st = i % stages;
+            mbar_wait(&empty[st], ((i / stages) & 1) ^ 1);
+            mbar_expect_tx(&full[st], chunk);
+            const int tile = t0 + (int)(i / (kbs / kbox)), kb = (int)(i % (kbs / kbox)) * kbox;
+            tma_load_4d_hint(sm + (size_t)st * chunk, &map, &full[st], 0, 0, kb, tile, policy_evict_first());
+        }
+    } else if (threadIdx.x == 32) {
+        unsigned long long acc = 0;
+        for (long long i = 0; i < n; ++i) {
+            const int st = i % stages;
+            mbar_wait(&full[st], (i / stages) & 1);
+            acc += sm[(size_t)st * chunk];
+            mbar_arrive(&empty[st]);
+        }
+        if (acc == 0xdeadbeef) *sink = acc;
+    }
+}
 
 __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -92,26 +130,43 @@ int main() {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaFuncSetAttribute(stream_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(stream_tma4d, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    const int K = 896, nt = int(total / (size_t(128) * K * 2));
+    CUtensorMap maps[3];
+    for (int kb : {1, 2, 4}) make_tmap_packed(&maps[kb == 1 ? 0 : kb == 2 ? 1 : 2], buf, nt * 128, K, 1, kb);
     for (int G : {16, 148}) {
-        const size_t per = (total / G) & ~size_t(65535);
-        auto run = [&](auto kern, int threads, const char* name) {
-            for (int rep = 0; rep < 2; ++rep) {
+        for (int kb : {1, 2, 4})
+            for (int stages : {3, 4, 6, 8}) {
+                const int chunk = kb * 16384;
+                if ((size_t)stages * chunk > 200 * 1024 || (K / 64) % kb) continue;
+                const int smem = stages * chunk + 2 * stages * 8 + 64;
+                CUtensorMap m = maps[kb == 1 ? 0 : kb == 2 ? 1 : 2];
+                stream_tma4d<<<G, 64, smem>>>(m, nt, K / 64, kb, stages, sink);
                 cudaEventRecord(a);
-                kern<<<G, threads>>>(reinterpret_cast<const uint4*>(buf), per / 16, sink);
+                stream_tma4d<<<G, 64, smem>>>(m, nt, K / 64, kb, stages, sink);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms;
+                cudaEventElapsedTime(&ms, a, b);
+                const double gbs = double(nt) * 128 * K * 2 / (ms * 1e-3) / 1e9;
+                printf("tma4d G=%3d box=%d kb (%5d B) stages=%d  %7.1f GB/s  %6.1f GB/s/SM\n", G, kb, chunk, stages, gbs,
+                       gbs / G);
+            }
+        const size_t per = (total / G) & ~size_t(65535);
+        for (int chunk : {16384, 32768, 65536})
+            for (int stages : {3, 4, 6}) {
+                if ((size_t)stages * chunk > 200 * 1024) continue;
+                const int smem = stages * chunk + 2 * stages * 8;
+                stream_bulk<<<G, 64, smem>>>(buf, per, chunk, stages, sink, 1);
+                cudaEventRecord(a);
+                stream_bulk<<<G, 64, smem>>>(buf, per, chunk, stages, sink, 1);
                 cudaEventRecord(b);
                 cudaEventSynchronize(b);
                 float ms;
                 cudaEventElapsedTime(&ms, a, b);
                 const double gbs = per * (double)G / (ms * 1e-3) / 1e9;
-                if (rep) printf("ldg G=%3d %-22s %7.1f GB/s  %6.1f GB/s/SM\n", G, name, gbs, gbs / G);
+                printf("bulk  G=%3d chunk=%6d stages=%d  %7.1f GB/s  %6.1f GB/s/SM\n", G, chunk, stages, gbs, gbs / G);
             }
-        };
-        run(stream_ldg<8, 256>, 256, "256 thr x 8 (32 KB)");
-        run(stream_ldg<16, 256>, 256, "256 thr x 16 (64 KB)");
-        run(stream_ldg<8, 512>, 512, "512 thr x 8 (64 KB)");
-        run(stream_ldg<16, 512>, 512, "512 thr x 16 (128 KB)");
-        run(stream_ldg<8, 1024>, 1024, "1024 thr x 8 (128 KB)");
-        run(stream_ldg<12, 1024>, 1024, "1024 thr x 12 (192 KB)");
     }
     printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
