@@ -18,7 +18,7 @@ import bench  # noqa: E402
 from paper_2603_10342_b200.agsv import Agsv  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--config", choices=["c2", "c3"], default="c2")
+ap.add_argument("--config", choices=["c2", "c3", "c4"], default="c2")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--out", default=None)
 ap.add_argument("--policies", nargs="*", default=None, help="subset, e.g. agentserve mixed_fcfs static_partition:3")
@@ -29,7 +29,18 @@ api = Agsv()
 if a.config == "c2":
     doc, src = bench.profile_doc(api)
     base = bench.workload_config(1, 0, "wall", "agentserve", doc)
-else:  # C3: Llama-3.2-3B-shaped, 32 ReAct agents, shaped profile
+elif a.config == "c4":  # C4: Qwen2.5-7B-shaped, 64 agents, 8k system prompts
+    prof = ROOT / "profiles" / "b200_profile_qwen2.5-7b.json"
+    d = json.loads(prof.read_text())
+    d.pop("measured", None)
+    base = {"workload": {"paradigm": "react", "model": "qwen2.5-7b", "concurrency": 64,
+                         "cold": {"min": 8192, "max": 8192, "mean": 8192},
+                         "resume": {"min": 256, "max": 256, "mean": 256}},
+            "slo": {"factor": 8.0, "tpot_stat": "p95"}, "policy": "agentserve", "seed": 13,
+            "profile": {"inline": d},
+            "backend": {"clock": "wall", "model": "qwen2.5-7b", "device": 0, "prefill_unit_tokens": 2048}}
+    src = str(prof.relative_to(ROOT))
+else:  # C3: Llama-3.2-3B-shaped, 32 ReAct agents
     prof = ROOT / "profiles" / "b200_profile_llama3.2-3b.json"
     d = json.loads(prof.read_text())
     d.pop("measured", None)
