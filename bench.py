@@ -155,7 +155,8 @@ def _episode_stats(recs: list[dict]) -> dict:
             "n_steps": len(steps),
             "prefill_tokens": sum(r["len"] for r in recs if r.get("k") == "prefill_done" and r.get("ctx") != "decode"),
             "chunk_tokens": sum(s.get("chunk", 0) for s in steps),
-            "batch_sizes": [s["batch"] for s in steps]}
+            "batch_sizes": [s["batch"] for s in steps],
+            "step_sms": [(s.get("sms", 0), s.get("dev_ms", 0.0)) for s in steps]}
 
 
 _ORACLE = {}
@@ -402,6 +403,16 @@ def run_mine(args) -> None:
                             "avg_launch_us": round(1000.0 * dom["ms"] / max(1, dom["launches"]), 2),
                             "share_of_device_time": round(dom["ms"] / sum(v["ms"] for v in kern.values()), 3),
                             "measured": "profiled replay of the timed episode (CUDA events per launch)"}
+        # context: the decode lane runs on a Green Context partition; a partition of n SMs can
+        # stream at most ~119 GB/s per SM with 32 KiB TMA requests (scripts/probes/stream.cu,
+        # profiles/r1_stream_probe_ldg.txt), so the attainable decode bandwidth is below HBM peak
+        sms_w = [(n, ms) for s in stats for n, ms in s.get("step_sms", []) if n > 0 and ms > 0]
+        if sms_w and hbm:
+            mean_sms = sum(n * ms for n, ms in sms_w) / sum(ms for _, ms in sms_w)
+            ceil = min(peaks["hbm"], 119.0 * mean_sms)
+            line["roofline"]["decode_sms_mean"] = round(mean_sms, 1)
+            line["roofline"]["partition_ceiling_gbs"] = round(ceil, 1)
+            line["roofline"]["frac_of_partition_ceiling"] = round(achieved / ceil, 4)
         da = cats.get("decode_attn")
         if da and da["ms"] > 0:
             line["decode_attn"] = {"achieved_gbs": round(da["units"] / (da["ms"] / 1000.0) / 1e9, 1),
