@@ -36,17 +36,24 @@ def main():
     ap.add_argument("--models", nargs="*", default=list(CASES))
     ap.add_argument("--out", default="gpurun_out/kernels.json")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--decode", nargs="*", default=None, help="override decode cases, e.g. 16x3000 48x3000")
+    ap.add_argument("--no-prefill", action="store_true")
     a = ap.parse_args()
     results = []
     rng = np.random.default_rng(0)
     for name in a.models:
         pls, dcs = CASES[name]
+        if a.decode:
+            dcs = [tuple(int(v) for v in c.split("x")) for c in a.decode]
+        if a.no_prefill:
+            pls = []
         max_ctx = max([p for p in pls] + [c for _, c in dcs]) + 256
+        pmax = max(pls + [256])
         m = Model(name, seed=13, max_context=max_ctx)
         V = m.vocab
-        nb = sum((c + 63) // 64 + 1 for b, c in dcs for _ in range(b)) + 2 * (max(pls) // 64 + 2)
+        nb = sum((c + 63) // 64 + 1 for b, c in dcs for _ in range(b)) + 2 * (pmax // 64 + 2)
         kv = KvPool(m, num_blocks=nb)
-        lane = Lane(m, max_tokens=max(pls + [256]), max_segments=80)
+        lane = Lane(m, max_tokens=pmax, max_segments=80)
         # prefill
         for L in pls:
             for rep in range(a.reps + 1):
@@ -70,7 +77,7 @@ def main():
             for s in sess:
                 done = 0
                 while done < ctx - 1:
-                    n = min(lane_max := max(pls + [256]), ctx - 1 - done)
+                    n = min(pmax, ctx - 1 - done)
                     lane.forward(kv, [(s, n, 0)], rng.integers(0, V, n))
                     done += n
             lane.wait()
