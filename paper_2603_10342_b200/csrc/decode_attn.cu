@@ -498,7 +498,7 @@ cudaError_t decode_attention(const CUtensorMap& tmap_k32, const CUtensorMap& tma
     // the cluster merge (launch_hd) takes up to 8 splits: a portable cluster
     static const bool no_cluster = std::getenv("ASB_ATTN_NO_CLUSTER") != nullptr;
     static const int force = std::getenv("ASB_DECODE_SPLITS") ? std::atoi(std::getenv("ASB_DECODE_SPLITS")) : 0;
-    const int splits0 = force > 0 ? force
+    const int splits0 = force > 0 ? std::min(force, max_splits)  // partial buffers hold max_splits
                                   : decode_splits(n_items, s.hkv, max_ctx, num_sms,
                                                   no_cluster ? max_splits : std::min(max_splits, 8));
     const int subs = (max_ctx + kSub - 1) / kSub;

@@ -1,0 +1,38 @@
+"""Every split-KV merge path of paged decode attention against the CPU oracle.
+
+The default split rule (decode_splits, csrc/decode_attn.cu) picks one path per shape; the
+others stay reachable through runtime switches and must give the same
+answer.  Each variant re-runs the head_dim-128 case of test_forward_matches_oracle (2500 /
+1300-token contexts, GQA group 3) in a fresh process, because the switches are read once
+per process:
+  forced 3 splits       -> 3-CTA thread-block cluster, DSMEM merge (odd cluster size)
+  no cluster, 16 splits -> fp32 partials merged by the grid's last-arriving CTA per row
+  combine kernel        -> fp32 partials merged by decode_combine_kernel
+  1 split               -> no merge at all on long contexts
+"""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+CASE = "tests/test_forward_gpu.py::test_forward_matches_oracle[hd128-prompt_lens2-6]"
+
+
+@pytest.mark.parametrize("env", [
+    {"ASB_DECODE_SPLITS": "3"},
+    {"ASB_ATTN_NO_CLUSTER": "1", "ASB_DECODE_SPLITS": "16"},
+    {"ASB_ATTN_COMBINE": "1", "ASB_ATTN_NO_CLUSTER": "1"},
+    {"ASB_DECODE_MAX_SPLITS": "1"},
+], ids=["cluster3", "last_arriver16", "combine", "single"])
+def test_decode_attention_merge_paths(env):
+    e = dict(os.environ)
+    e.update(env)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", CASE],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "1 passed" in r.stdout
