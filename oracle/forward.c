@@ -16,7 +16,11 @@
  * points as the device path.  What IS pinned to the reference: the splitmix64 named
  * sub-stream generator used for weights and token ids (src/rng.hpp:14-60, restated below and
  * checked against the compiled reference in tests), and — through oracle/_ref — every
- * scheduling decision and KV prefix length.
+ * scheduling decision and KV prefix length.  The decoder math itself is pinned to an
+ * independent public implementation instead: tests/test_oracle_pin_hf.py runs these weights
+ * (fo_tensor) through transformers 5.5.0's Llama / Qwen2 modelling code in fp32 and bounds
+ * the logit difference at 1% (measured 0.3-0.5%; a wrong RoPE theta, Llama-3 frequency
+ * scaling or KV-head grouping exceeds it).
  *
  * Numerics contract (identical on device):
  *   x0 = embed[tok]                                   (bf16)
@@ -204,6 +208,29 @@ void fo_free(fo_model* m) {
     free(m->cos_t);
     free(m->sin_t);
     free(m);
+}
+
+const float* fo_tensor(const fo_model* m, int layer, const char* name, int64_t* n) {
+    const fo_spec* s = &m->s;
+    const int64_t qd = (int64_t)s->hq * s->hd, kvd = (int64_t)s->hkv * s->hd, d = s->d, f = s->ffn;
+    if (!strcmp(name, "embed")) { *n = (int64_t)s->vocab * d; return m->embed; }
+    if (!strcmp(name, "lm_head")) { *n = (int64_t)s->vocab * d; return m->lm_head; }
+    if (!strcmp(name, "final_norm")) { *n = d; return m->final_norm; }
+    if (layer < 0 || layer >= m->n_layers) return NULL;
+    const fo_layer* L = &m->layers[layer];
+    if (!strcmp(name, "attn_norm")) { *n = d; return L->attn_norm; }
+    if (!strcmp(name, "mlp_norm")) { *n = d; return L->mlp_norm; }
+    if (!strcmp(name, "q")) { *n = qd * d; return L->wq; }
+    if (!strcmp(name, "k")) { *n = kvd * d; return L->wk; }
+    if (!strcmp(name, "v")) { *n = kvd * d; return L->wv; }
+    if (!strcmp(name, "q_bias")) { *n = qd; return L->bq; }
+    if (!strcmp(name, "k_bias")) { *n = kvd; return L->bk; }
+    if (!strcmp(name, "v_bias")) { *n = kvd; return L->bv; }
+    if (!strcmp(name, "o")) { *n = d * qd; return L->wo; }
+    if (!strcmp(name, "gate")) { *n = f * d; return L->wg; }
+    if (!strcmp(name, "up")) { *n = f * d; return L->wu; }
+    if (!strcmp(name, "down")) { *n = d * f; return L->wd; }
+    return NULL;
 }
 
 fo_session* fo_session_new(fo_model* m) {

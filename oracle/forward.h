@@ -19,6 +19,10 @@ fo_model* fo_create(const fo_spec* spec, uint64_t seed, int max_ctx, int n_layer
 void fo_free(fo_model* m);
 /* bf16 bits of a named weight tensor element (same generator as the device init) */
 uint16_t fo_weight_bits(uint64_t seed, const char* name, int64_t index, float offset, float amp);
+/* Read-only view of a generated weight tensor (fp32 holding bf16 values): name is one of
+ * embed, lm_head, final_norm, or a per-layer attn_norm, mlp_norm, q, k, v, q_bias, k_bias,
+ * v_bias, o, gate, up, down; *n receives the element count.  NULL if absent. */
+const float* fo_tensor(const fo_model* m, int layer, const char* name, int64_t* n);
 fo_session* fo_session_new(fo_model* m);
 void fo_session_free(fo_session* s);
 int fo_session_len(const fo_session* s);

@@ -38,6 +38,8 @@ def lib():
         L.fo_free.argtypes = [C.c_void_p]
         L.fo_weight_bits.restype = C.c_uint16
         L.fo_weight_bits.argtypes = [C.c_uint64, C.c_char_p, C.c_int64, C.c_float, C.c_float]
+        L.fo_tensor.restype = C.POINTER(C.c_float)
+        L.fo_tensor.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.POINTER(C.c_int64)]
         L.fo_session_new.restype = C.c_void_p
         L.fo_session_new.argtypes = [C.c_void_p]
         L.fo_session_free.argtypes = [C.c_void_p]
@@ -90,6 +92,14 @@ class OracleModel:
         self.spec = make_spec(spec)
         self.h = lib().fo_create(C.byref(self.spec), seed, max_ctx, layers_limit)
         self.seed = seed
+
+    def tensor(self, name: str, layer: int = -1) -> np.ndarray:
+        """Copy of a generated weight tensor (fp32 holding bf16 values), flat."""
+        n = C.c_int64(0)
+        ptr = lib().fo_tensor(self.h, layer, name.encode(), C.byref(n))
+        if not ptr:
+            raise KeyError(name)
+        return np.ctypeslib.as_array(ptr, shape=(n.value,)).copy()
 
     def session(self) -> "OracleSession":
         return OracleSession(self)
