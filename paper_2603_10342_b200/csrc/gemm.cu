@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty_bar = full_bar + C::kStages;
     uint64_t* tfull_bar = empty_bar + C::kStages;
     uint64_t* tempty_bar = tfull_bar + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    uint64_t* recv_bar = tempty_bar + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
     float* part = reinterpret_cast<float*>(smem);  // cluster split-K partial [BN][128]
 
     const uint32_t warp = warp_id();
@@ -193,6 +194,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     // staged swap epilogue: the tile's fp32 partial is parked in smem and finished from there
     // (cluster split-K reduction over DSMEM, and/or the cross-row QKV/RoPE epilogue)
     const bool clustered = p.swap && (p.splits > 1 || p.epi == EPI_QKV);
+    // Split-K reduction by bulk push: CTA r of the S-CTA cluster finishes the weight rows of
+    // slice r (4-row units, [ro(r), ro(r+1))); every CTA parks its partial slice-major
+    // ([slice][token][row]) and pushes slice q to CTA q with one cp.async.bulk smem->DSMEM
+    // copy, landing in q's (now idle) operand ring; q sums the S slices from local smem in
+    // rank order (the pull reduction's order: bit-identical).  The QKV/RoPE epilogue needs
+    // row pairs (j, j + hd/2) from different slices and keeps the DSMEM-load reduction.
+    const int S_ = p.splits > 1 ? p.splits : 1;
+    // (from 32 tokens: below that the DSMEM loads are few and the copy + fence latency loses)
+    const bool bulk = clustered && S_ > 1 && p.epi != EPI_QKV && !p.reduce_pull && BN <= 128 && p.tokens >= 32;
+    const int Tp = p.tokens < BN ? p.tokens : BN;
+    auto ro = [&](int r) { return 4 * ((32 * r) / S_); };
     auto stamp = [&](int k) {
         if (p.dbg_times) {
             unsigned long long t;
@@ -213,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tfull_bar[b], 1);
             mbar_init(&tempty_bar[b], 128);
         }
+        mbar_init(recv_bar, 1);
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -354,14 +367,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int m = tm * BM + row_in_tile;
             const uint32_t t_row = tmem_base + ((quarter * 32u) << 16) + ab * BN;
             if (clustered) {
-                // park the partial: part[tok][row], lanes = consecutive rows (conflict-free);
-                // every MMA of this CTA has completed, so the operand ring is free
+                // park the partial: part[tok][row] (pull) or slice-major (bulk), lanes =
+                // consecutive rows (conflict-free); every MMA of this CTA has completed, so the
+                // operand ring is free
+                int sr = 0;
+                while (bulk && sr + 1 < S_ && ro(sr + 1) <= static_cast<int>(row_in_tile)) ++sr;
+                const int r0 = bulk ? ro(sr) : 0;
+                const int stride = bulk ? ro(sr + 1) - r0 : BM;
+                float* dst = part + (bulk ? Tp * r0 : 0) + (row_in_tile - r0);
                 for (int c = 0; c < BN && c < p.tokens; c += 32) {
                     uint32_t r[32];
                     tmem_ld32(t_row + c, r);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) part[(c + j) * BM + row_in_tile] = __uint_as_float(r[j]);
+                    for (int j = 0; j < 32; ++j)
+                        if (!bulk || c + j < Tp) dst[(c + j) * stride] = __uint_as_float(r[j]);
                 }
                 continue;
             }
@@ -566,7 +586,100 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (threadIdx.x == 64) stamp(2);
     tc_fence_before();
-    if (clustered) {
+    if (clustered && bulk) {
+        Epi epi{p};
+        const int rank = blockIdx.x % S_;
+        const int tile = blockIdx.x / S_;
+        const int r0 = ro(rank), nr = ro(rank + 1) - r0, nu = nr / 4;
+        const uint32_t part_s = smem_u32(part);
+        const uint32_t recv_s = part_s + BM * BN * 4;  // S slots of [Tp][nr] fp32
+        const uint32_t slot_bytes = static_cast<uint32_t>(Tp * nr * 4);
+        fence_proxy_async_smem();  // parked partial -> visible to the bulk-copy engine
+        if (threadIdx.x == 0) mbar_expect_tx(recv_bar, (S_ - 1) * slot_bytes);
+        cluster_sync();  // every CTA has parked its partial and armed its receive barrier
+        if (threadIdx.x == 0) {
+            stamp(7);
+            for (int q = 0; q < S_; ++q) {
+                if (q == rank) continue;
+                const int q0 = ro(q);
+                const uint32_t bytes = static_cast<uint32_t>(Tp * (ro(q + 1) - q0) * 4);
+                bulk_s2cluster(mapa_shared(recv_s + rank * bytes, q), part_s + Tp * q0 * 4, bytes,
+                               mapa_shared(smem_u32(recv_bar), q));
+            }
+        }
+        const int n_el = Tp * nu;
+        const int m_base = (tile % tiles_m) * BM + r0;
+        const bool vec_r = (p.ldr & 3) == 0, vec_o = (p.ldo & 3) == 0;
+        constexpr int CH = 4;
+        for (int e0 = threadIdx.x, round = 0; round == 0 || e0 < n_el; e0 += kThreads * CH, ++round) {
+            // residual rows first: their HBM/L2 latency overlaps the incoming copies
+            float rr[CH][4];
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int e = e0 + c * kThreads;
+                rr[c][0] = rr[c][1] = rr[c][2] = rr[c][3] = 0.f;
+                if (p.epi != EPI_RESID || e >= n_el) continue;
+                const int tok = e / nu, m = m_base + 4 * (e % nu);
+                const __nv_bfloat16* rp = p.resid + static_cast<size_t>(tok) * p.ldr + m;
+                if (vec_r && m + 3 < p.n_out) {
+                    const uint2 w = *reinterpret_cast<const uint2*>(rp);
+                    rr[c][0] = bf16_lo(w.x), rr[c][1] = bf16_hi(w.x), rr[c][2] = bf16_lo(w.y), rr[c][3] = bf16_hi(w.y);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (m + k < p.n_out) rr[c][k] = __bfloat162float(rp[k]);
+                }
+            }
+            if (round == 0) {
+                mbar_wait(recv_bar, 0);
+                cluster_arrive();  // all our incoming copies landed: peers may exit after this
+            }
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int e = e0 + c * kThreads;
+                if (e >= n_el) continue;
+                const int tok = e / nu, u = e % nu;
+                const uint32_t off = static_cast<uint32_t>((tok * nr + 4 * u) * 4);
+                float4 v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q < S_) v[q] = lds128f(q == rank ? part_s + Tp * r0 * 4 + off : recv_s + q * slot_bytes + off);
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q < S_) {
+                        a0 += v[q].x;
+                        a1 += v[q].y;
+                        a2 += v[q].z;
+                        a3 += v[q].w;
+                    }
+                const int m = m_base + 4 * u;
+                if (p.epi == EPI_RESID) {
+                    const float y[4] = {a0 + rr[c][0], a1 + rr[c][1], a2 + rr[c][2], a3 + rr[c][3]};
+                    __nv_bfloat16* op = p.out + static_cast<size_t>(tok) * p.ldo + m;
+                    if (vec_o && m + 3 < p.n_out) {
+                        *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]));
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (m + k < p.n_out) op[k] = __float2bfloat16_rn(y[k]);
+                    }
+                } else {
+                    epi.store_pair(tok, m, a0, a1);
+                    epi.store_pair(tok, m + 2, a2, a3);
+                }
+                if (p.amax) {
+                    const float a[4] = {a0, a1, a2, a3};
+                    unsigned long long k = 0ull;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (m + i < p.n_out) k = max(k, argmax_key(a[i], m + i));
+                    if (k) atomicMax(p.amax + tok, k);
+                }
+            }
+        }
+        cluster_wait();  // every CTA has received: no copy still reads our partial
+    } else if (clustered) {
         // Reduce the tile over the cluster: CTA `rank` finishes row pairs
         // [64*rank/S, 64*(rank+1)/S), summing the S partials in rank order.
         cluster_sync();

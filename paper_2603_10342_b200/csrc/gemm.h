@@ -58,6 +58,7 @@ struct GemmParams {
                                // (atomicMax; zero on entry) -- the LM head's greedy sample
     unsigned long long* dbg_times;  // optional per-CTA timeline [grid][8] (globaltimer ns)
     PostNorm post;                  // optional, EPI_RESID
+    int reduce_pull;                // cluster split-K: DSMEM loads by the owner (A/B switch) instead of bulk push
     int dbg_no_epi;                 // timing ablation: epilogue drains TMEM but stores nothing
 };
 

@@ -469,6 +469,8 @@ void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
     p.dbg_times = L->dbg_times;
     static const bool no_epi = std::getenv("ASB_GEMM_NO_EPI") != nullptr;  // timing ablation only
     p.dbg_no_epi = no_epi ? 1 : 0;
+    static const bool pull = std::getenv("ASB_GEMM_PULL_REDUCE") != nullptr;  // A/B: DSMEM-load reduce
+    p.reduce_pull = pull ? 1 : 0;
     const int num_sms = L->n_sms();
     L->n_launch += 1;
     const bool swap = force_path >= 0 ? force_path == 1 : T <= 256;

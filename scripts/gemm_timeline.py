@@ -16,6 +16,8 @@ L.asb_debug_gemm_timeline.argtypes = [C.c_void_p, C.POINTER(C.c_ulonglong), C.c_
 EPI = {"bf16": 0, "resid": 1, "silu": 2, "f32": 3}
 SHAPES = {"8b": [("qkv", 6144, 4096, "bf16"), ("o", 4096, 4096, "resid"), ("gate_up", 28672, 4096, "silu"),
                 ("down", 4096, 14336, "resid")],
+          "3b": [("qkv", 5120, 3072, "bf16"), ("o", 3072, 3072, "resid"), ("gate_up", 16384, 3072, "silu"),
+                 ("down", 3072, 8192, "resid")],
           "0.5b": [("qkv", 1152, 896, "bf16"), ("o", 896, 896, "resid"), ("gate_up", 9728, 896, "silu"),
                   ("down", 896, 4864, "resid"), ("lm_head", 151936, 896, "f32")]}
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 64

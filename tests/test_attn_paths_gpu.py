@@ -36,3 +36,16 @@ def test_decode_attention_merge_paths(env):
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "1 passed" in r.stdout
+
+
+def test_gemm_pull_reduction_switch():
+    """The DSMEM-load split-K reduction (ASB_GEMM_PULL_REDUCE=1, the A/B baseline of the bulk
+    push) stays correct on the cluster cases."""
+    e = dict(os.environ)
+    e["ASB_GEMM_PULL_REDUCE"] = "1"
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        "tests/test_gemm_gpu.py", "-k", "3072-1024-1-5 or 1000-640-1-6 or 896-896-1-7 or 512-256-1-3"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "16 passed" in r.stdout, r.stdout[-500:]
+

@@ -28,6 +28,8 @@ def _ref(x, w, bias, resid, epi):
     (300, 896, 896, 0, 0), (1024, 1152, 896, 0, 0), (2048, 4096, 512, 0, 0),
     (8, 1152, 896, 1, 0), (80, 896, 4864, 1, 0), (33, 4096, 1024, 1, 1), (200, 512, 256, 1, 3),
     (130, 256, 704, 0, 0), (1, 4096, 256, 1, 0),
+    # cluster split-K at >= 32 tokens: bulk-push reduction (ragged N, odd token counts)
+    (64, 3072, 1024, 1, 5), (45, 1000, 640, 1, 6), (32, 896, 896, 1, 7),
     # path 2: small-batch dgemv (legacy warp MMA fed from HBM), T <= 32, ragged N
     (1, 4096, 256, 2, 0), (8, 1152, 896, 2, 0), (13, 896, 4864, 2, 0), (16, 9728, 896, 2, 0),
     (24, 512, 256, 2, 0), (32, 1000, 640, 2, 0), (5, 136, 3072, 2, 0),
