@@ -273,6 +273,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else
                     tma_load_2d_hint(smem_a + stage * C::kBytesA, &tmap_a, &full_bar[stage], kb * BK, tm * BM, pol_x);
             };
+            // Swap path: the smem ring holds only a few units of the weight stream, so on a small
+            // partition the in-flight bytes per SM (not HBM) bound the rate.  Prefetch the
+            // weight stream l2_pf units ahead of the TMA loads into L2 (no smem needed).
+            const int pf = (p.swap && p.a_packed && p.w_packed) ? p.l2_pf : 0;
+            auto pf_w = [&](int kb, int tm) {
+                const int k0 = kb * KP;
+                const int nk = min(KP, p.w_kblocks - k0);
+                if (nk <= 0) return;
+                prefetch_l2_bulk(p.w_packed + (static_cast<size_t>(tm) * p.w_kblocks + k0) * (BM * BK),
+                                 static_cast<uint32_t>(nk * BM * BK * 2));
+            };
             Work w;
             w.init(p, tiles_m, tiles_n, k_blocks);
             // Weights do not depend on the previous kernel: fill the first ring with weight
@@ -286,6 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_expect_tx(&full_bar[pre], C::kStageBytes);
                         load_w(pre, kb, tm, tn);
                     }
+                    for (int kb = kb0 + pre; kb < kb1 && kb < kb0 + pre + pf; ++kb) pf_w(kb, tm);
                 }
             }
             pdl_wait();
@@ -295,6 +307,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             while (w.next(tm, tn, kb0, kb1)) {
                 for (int kb = kb0; kb < kb1; ++kb, ++i) {
                     if (i >= pre) {
+                        if (pf) {
+                            if (kb == kb0)  // a later tile of a persistent CTA: open its window
+                                for (int u = kb0 + 1; u < kb1 && u < kb0 + pf; ++u) pf_w(u, tm);
+                            if (kb + pf < kb1) pf_w(kb + pf, tm);
+                        }
                         mbar_wait(&empty_bar[stage], phase ^ 1);
                         mbar_expect_tx(&full_bar[stage], C::kStageBytes);
                         load_w(stage, kb, tm, tn);

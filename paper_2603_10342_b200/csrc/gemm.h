@@ -58,6 +58,9 @@ struct GemmParams {
                                // (atomicMax; zero on entry) -- the LM head's greedy sample
     unsigned long long* dbg_times;  // optional per-CTA timeline [grid][8] (globaltimer ns)
     PostNorm post;                  // optional, EPI_RESID
+    const __nv_bfloat16* w_packed;  // swap: the tile-packed weight (for L2 prefetch-ahead)
+    int w_kblocks;                  // its 64-wide k-blocks per 128-row tile
+    int l2_pf;                      // swap: L2 prefetch distance in pipeline units (0 = off)
     int reduce_pull;                // cluster split-K: DSMEM loads by the owner (A/B switch) instead of bulk push
     int dbg_no_epi;                 // timing ablation: epilogue drains TMEM but stores nothing
 };

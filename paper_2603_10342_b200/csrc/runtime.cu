@@ -485,6 +485,12 @@ void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
         const int bn = gemm_pick_bn(T);
         p.swap = 1;
         p.a_packed = 1;
+        p.w_packed = w.ptr;
+        p.w_kblocks = w.cols / 64;
+        // L2 prefetch-ahead of the weight stream: measured slower (+5-8% per decode step at
+        // 16-148 SMs, profiles/r1_gemm_l2_prefetch_ab.txt), off unless ASB_GEMM_L2PF=<units>
+        static const int l2pf = std::getenv("ASB_GEMM_L2PF") ? std::atoi(std::getenv("ASB_GEMM_L2PF")) : 0;
+        p.l2_pf = l2pf;
         p.M = w.rows;
         p.N = T;
         const int tiles = (w.rows + 127) / 128;
