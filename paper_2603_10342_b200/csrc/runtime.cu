@@ -499,7 +499,8 @@ void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
         const int kp = (bn <= 64 && !kp1) ? 2 : 1;
         const int kb = ((w.cols + 63) / 64 + kp - 1) / kp;
         // fewer weight tiles than SMs: split K over an S-CTA cluster per tile (DSMEM reduce)
-        p.splits = gemm_cluster_splits(tiles, kb, bn, num_sms, L->stream, force_splits, kp);
+        static const int env_splits = std::getenv("ASB_GEMM_SPLITS") ? std::atoi(std::getenv("ASB_GEMM_SPLITS")) : 0;
+        p.splits = gemm_cluster_splits(tiles, kb, bn, num_sms, L->stream, force_splits ? force_splits : env_splits, kp);
         e = kp == 2 ? gemm_launch(w.map_a128k2, xmaps[bn == 32 ? 5 : 6], p, bn, num_sms, L->stream, pdl, 2)
                     : gemm_launch(w.map_a128, xmaps[swap_map_index(bn)], p, bn, num_sms, L->stream, pdl);
     } else {
