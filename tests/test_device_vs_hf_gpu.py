@@ -1,13 +1,14 @@
-"""The device forward at the C2 model's full shape (Qwen2.5-0.5B: 24 layers, GQA 7, q/k/v
-bias, tied 151936-token head) against transformers' Qwen2 modelling code in fp32 on the same
-GPU, with the same generated weights, at C2's context lengths (a 2300-token and a 700-token
-prompt in one ragged prefill batch, then teacher-forced decode steps of both rows).
+"""The device forward at full model shape against transformers' modelling code in fp32 on the
+same GPU, with the same generated weights, at the BASELINE configs' context lengths (two
+prompts in one ragged prefill batch, then teacher-forced decode steps of both rows):
+  C2 Qwen2.5-0.5B (24 layers, GQA 7, hd 64, q/k/v bias, tied 151936-token head), 2300 + 700;
+  C3 Llama-3.2-3B (28 layers, GQA 3, hd 128, Llama-3 RoPE scaling, tied head), 3000 + 500.
 
 This exercises the paths the small oracle cases cannot: long-context split-KV decode
 attention, multi-tile GQA-packed prefill attention, and the decode GEMM paths the real
 model's shapes select.  Tolerances are the device-vs-oracle ones of tests/test_forward_gpu.py
 (bf16 storage against an fp32 reference); measured on a B200: max error 1.45% of max|logit|,
-rel-L2 1.39%, greedy ids identical.
+rel-L2 1.39% (0.5B); 4.86% / 4.60% (3B, see TOL); greedy ids identical in both.
 """
 import numpy as np
 import pytest
@@ -19,21 +20,26 @@ pytest.importorskip("transformers")
 
 pytestmark = pytest.mark.gpu
 
-LOGIT_ATOL_FRAC = 0.03
-LOGIT_RL2 = 0.02
+# (max |err| / max |logit|, rel-L2).  3B: the CPU oracle — the device's own bf16 rounding
+# points, fp32 accumulation — is itself 2.8-3.8% from transformers' fp32 forward at every
+# prompt length (64-3000 tokens, scripts/hf_diag.py, profiles/r1_hf_diag_3b.txt): bf16
+# activation rounding amplified through 28 random-weight layers.  The device sits at the same
+# distance (3.6-4.3%), so the 3B bound is that noise floor plus margin, not a looser kernel.
+TOL = {"qwen2.5-0.5b": (0.03, 0.02), "llama3.2-3b": (0.06, 0.06)}
 
 
-def test_qwen05b_device_matches_transformers_at_c2_lengths():
+@pytest.mark.parametrize("name,lens", [("qwen2.5-0.5b", (2300, 700)), ("llama3.2-3b", (3000, 500))])
+def test_device_matches_transformers_at_config_lengths(name, lens):
+    LOGIT_ATOL_FRAC, LOGIT_RL2 = TOL[name]
     from paper_2603_10342_b200.device import KvPool, Lane, Model
     from tests.test_oracle_pin_hf import _hf_model
 
     seed = 13
-    lens = (2300, 700)
     steps = 4
-    om = OracleModel("qwen2.5-0.5b", seed=seed, max_ctx=4096)
-    hf = _hf_model(om).cuda()
+    om = OracleModel(name, seed=seed, max_ctx=4096)
+    hf = _hf_model(om, device="cuda")
     del om
-    m = Model("qwen2.5-0.5b", seed=seed, max_context=4096)
+    m = Model(name, seed=seed, max_context=4096)
     kv = KvPool(m, num_blocks=2 * (4096 // 64) + 8)
     lane = Lane(m, max_tokens=4096, max_segments=8)
     V = m.vocab

@@ -36,7 +36,7 @@ SPECS = {
 }
 
 
-def _hf_model(om: OracleModel):
+def _hf_model(om: OracleModel, device: str = "cpu"):
     s = om.spec
     rope = {"rope_type": "default", "rope_theta": float(s.theta)}
     if s.rope_llama3:
@@ -47,12 +47,13 @@ def _hf_model(om: OracleModel):
                   num_attention_heads=s.hq, num_key_value_heads=s.hkv, head_dim=s.hd,
                   rms_norm_eps=float(s.eps), rope_parameters=rope, tie_word_embeddings=bool(s.tied),
                   max_position_embeddings=131072 if s.rope_llama3 else 4096)
-    if s.qkv_bias:
-        cfg = transformers.Qwen2Config(**common)
-        model = transformers.Qwen2ForCausalLM(cfg)
-    else:
-        cfg = transformers.LlamaConfig(attention_bias=False, mlp_bias=False, **common)
-        model = transformers.LlamaForCausalLM(cfg)
+    with torch.device(device):
+        if s.qkv_bias:
+            cfg = transformers.Qwen2Config(**common)
+            model = transformers.Qwen2ForCausalLM(cfg)
+        else:
+            cfg = transformers.LlamaConfig(attention_bias=False, mlp_bias=False, **common)
+            model = transformers.LlamaForCausalLM(cfg)
     cfg._attn_implementation = "eager"
     model = model.float().eval()
 
