@@ -22,7 +22,7 @@ pytestmark = pytest.mark.gpu
 
 # (max |err| / max |logit|, rel-L2).  3B: the CPU oracle — the device's own bf16 rounding
 # points, fp32 accumulation — is itself 2.8-3.8% from transformers' fp32 forward at every
-# prompt length (64-3000 tokens, scripts/hf_diag.py, profiles/r1_hf_diag_3b.txt): bf16
+# prompt length (64-3000 tokens, scripts/hf_diag.py, profiles/r1_hf_diag.txt): bf16
 # activation rounding amplified through 28 random-weight layers.  The device sits at the same
 # distance (3.6-4.3%), so the 3B bound is that noise floor plus margin, not a looser kernel.
 TOL = {"qwen2.5-0.5b": (0.03, 0.02), "llama3.2-3b": (0.06, 0.06)}
