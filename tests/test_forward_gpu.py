@@ -134,3 +134,24 @@ def test_forward_matches_oracle(spec, prompt_lens, steps):
                   m.info["layers"], m.info["n_kv_heads"] * m.info["head_dim"])
     n = stats["match"] + stats["near_tie"]
     assert stats["near_tie"] <= max(1, n // 10), stats
+
+
+def test_fused_argmax_matches_logits_at_40_rows():
+    """40 logit rows through the tiny model's LM head (32 weight tiles < SMs: cluster split-K,
+    >= 32 tokens: the bulk-push reduction) -- the fused greedy ids must be the argmax of the
+    fp32 logits the same launch writes (lowest index on ties), and the logits must match the
+    oracle's."""
+    m = Model("tiny", seed=5, max_context=1024)
+    kv = KvPool(m, num_blocks=128)
+    lane = Lane(m, max_tokens=1024, max_segments=48)
+    om = OracleModel("tiny", seed=5, max_ctx=1024)
+    n = 40
+    prompts = [token_stream(5, f"argmax/{i}", 7 + (i % 5), m.vocab) for i in range(n)]
+    lane.forward(kv, [(i, len(p), 1) for i, p in enumerate(prompts)], np.concatenate(prompts))
+    ids, lg = lane.fetch(n, logits=True)
+    for i, p in enumerate(prompts):
+        row = lg[i]
+        assert int(ids[i]) == int(np.flatnonzero(row == row.max())[0]), i
+        if i % 8 == 0:
+            _, clg = om.session().forward(p)
+            _cmp_logits(row, clg, f"row {i}")
