@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
+#include <vector>
 #include <cfloat>
 
 #include "attn.h"
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                              const PrefillItem* __restrict__ items,
                              const int32_t* __restrict__ tables, __nv_bfloat16* __restrict__ out,
                              float* __restrict__ part_o, float* __restrict__ part_ml,
-                             int blocks_per_split, const AttnShape s) {
+                             const int4* __restrict__ units, int blocks_per_split, const AttnShape s) {
     using C = PCfg<HD>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
@@ -99,20 +101,24 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint64_t* pv_done = p_full + 4;               // [2][2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 4);
 
-    // heaviest items (most causal pages) first: they define the tail
-    const int item_idx = gridDim.x - 1 - blockIdx.x;
+    // heaviest items (most causal pages) first: they define the tail.  Either a uniform split
+    // (grid.z splits of blocks_per_split pages) or a work-unit list (item, first page, pages,
+    // partial slot or -1): only the long causal items split, so the grid stays one wave.
+    const int4 unit = units ? units[gridDim.x - 1 - blockIdx.x] : make_int4(0, 0, 0, 0);
+    const int item_idx = units ? unit.x : static_cast<int>(gridDim.x - 1 - blockIdx.x);
     const PrefillItem it = items[item_idx];
     const int kvh = blockIdx.y;
     const int G = s.hq / s.hkv;
     const int tpt = 128 / G;          // tokens per tile
     const int box_rows = tpt * G;     // valid MMA rows of a full tile
     const int total_blocks = (it.q_pos0 + it.n_q + kBlockTokens - 1) / kBlockTokens;
-    const int blk0 = blockIdx.z * blocks_per_split;
-    const int n_kv = max(0, min(total_blocks, blk0 + blocks_per_split) - blk0);
-    const bool split = gridDim.z > 1;
+    const int blk0 = units ? unit.y : static_cast<int>(blockIdx.z) * blocks_per_split;
+    const int n_kv = max(0, min(total_blocks, blk0 + (units ? unit.z : blocks_per_split)) - blk0);
+    const bool split = units ? unit.w >= 0 : gridDim.z > 1;
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
-    const size_t pbase = (static_cast<size_t>(item_idx) * gridDim.y + kvh) * gridDim.z + blockIdx.z;
+    const size_t pbase = units ? static_cast<size_t>(unit.w < 0 ? 0 : unit.w) * gridDim.y + kvh
+                               : (static_cast<size_t>(item_idx) * gridDim.y + kvh) * gridDim.z + blockIdx.z;
     if (n_kv == 0) {
         // empty split: neutral partials
         for (int r = threadIdx.x; r < 256; r += blockDim.x) {
@@ -397,6 +403,36 @@ __global__ void prefill_combine_kernel(const PrefillItem* __restrict__ items,
         __float2bfloat16_rn(o / l);
 }
 
+// Merge the partials of the items the unit list split.  grid = (n_split_items, hkv, 256 / 8),
+// block = (HD, 8 rows); comb[i] = (item, first partial slot, slots).
+template <int HD>
+__global__ void prefill_combine_units_kernel(const PrefillItem* __restrict__ items, const int4* __restrict__ comb,
+                                             const float* __restrict__ part_o, const float* __restrict__ part_ml,
+                                             __nv_bfloat16* __restrict__ out, int hq, int hkv) {
+    pdl_trigger();
+    pdl_wait();
+    const int4 c = comb[blockIdx.x];
+    const PrefillItem it = items[c.x];
+    const int G = hq / hkv;
+    const int tpt = 128 / G;
+    const int prow = blockIdx.z * 8 + threadIdx.y, kvh = blockIdx.y, d = threadIdx.x;
+    const int t = prow / 128, rr = prow % 128;
+    const int tok = t * tpt + rr / G;
+    if (rr >= tpt * G || tok >= it.n_q) return;
+    float m = -FLT_MAX;
+    for (int q = 0; q < c.z; ++q) m = fmaxf(m, part_ml[((static_cast<size_t>(c.y + q) * hkv + kvh) * 256 + prow) * 2]);
+    float l = 0.f, o = 0.f;
+    for (int q = 0; q < c.z; ++q) {
+        const size_t row = (static_cast<size_t>(c.y + q) * hkv + kvh) * 256 + prow;
+        const float ls = part_ml[row * 2 + 1];
+        if (ls == 0.f) continue;
+        const float w = exp2f(part_ml[row * 2] - m);
+        l += ls * w;
+        o += part_o[row * HD + d] * w;
+    }
+    out[static_cast<size_t>(it.q_row0 + tok) * hq * HD + (kvh * G + rr % G) * HD + d] = __float2bfloat16_rn(o / l);
+}
+
 template <int HD>
 cudaError_t prefill_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                            const PrefillItem* items, int n_items, int max_blocks, int splits,
@@ -414,7 +450,7 @@ cudaError_t prefill_launch(const CUtensorMap& tq, const CUtensorMap& tk, const C
     splits = (max_blocks + bps - 1) / bps;
     dim3 grid(n_items, s.hkv, splits);
     cudaError_t e = launch_k(prefill_attention_kernel<HD>, grid, dim3(kPThreads), C::kSmem, stream, tq, tk, tv,
-                             items, tables, out, part_o, part_ml, bps, s);
+                             items, tables, out, part_o, part_ml, static_cast<const int4*>(nullptr), bps, s);
     if (e == cudaSuccess && splits > 1)
         e = launch_k(prefill_combine_kernel<HD>, dim3(n_items, s.hkv, 256), dim3(HD), 0, stream, items,
                      static_cast<const float*>(part_o), static_cast<const float*>(part_ml), splits, out, s.hq,
@@ -437,6 +473,74 @@ int prefill_splits(int n_items, int hkv, int max_blocks, int num_sms, size_t ws_
     splits = std::min(splits, 32);
     while (splits > 1 && static_cast<size_t>(ctas) * splits * 256 > ws_rows) --splits;
     return std::max(splits, 1);
+}
+
+int prefill_units(const PrefillItem* items, int n_items, int hkv, int num_sms, size_t ws_rows,
+                  std::vector<int4>& units, std::vector<int4>& comb) {
+    // One wave of CTAs (one per SM), the smallest per-CTA page budget B that fits: items with
+    // more than B causal pages split into balanced ranges, the rest run whole.  The tail of a
+    // causal batch is its longest item, so this shortens the critical path from max_i b_i to
+    // ~B pages where the uniform split could not (it splits every item or none).
+    units.clear();
+    comb.clear();
+    if (n_items <= 0 || n_items * hkv > num_sms) return 0;
+    std::vector<int> b(n_items);
+    int maxb = 0;
+    for (int i = 0; i < n_items; ++i) {
+        b[i] = (items[i].q_pos0 + items[i].n_q + kBlockTokens - 1) / kBlockTokens;
+        maxb = std::max(maxb, b[i]);
+    }
+    auto ctas = [&](int B) {
+        long long c = 0;
+        for (int i = 0; i < n_items; ++i) c += (b[i] + B - 1) / B;
+        return c * hkv;
+    };
+    int B = maxb;
+    while (B > 2 && ctas(B - 1) <= num_sms) --B;
+    if (B >= maxb) return 0;
+    int parts = 0;
+    for (int i = 0; i < n_items; ++i) {
+        const int n = (b[i] + B - 1) / B;
+        const int per = (b[i] + n - 1) / n;
+        if (n > 1) comb.push_back(make_int4(i, parts, n, 0));
+        for (int z = 0; z < n; ++z)
+            units.push_back(make_int4(i, z * per, std::min(per, b[i] - z * per), n > 1 ? parts + z : -1));
+        if (n > 1) parts += n;
+    }
+    if (static_cast<size_t>(parts) * hkv * 256 > ws_rows) {
+        units.clear();
+        comb.clear();
+        return 0;
+    }
+    return static_cast<int>(units.size());
+}
+
+cudaError_t prefill_attention_units(const CUtensorMap& tmap_q, const CUtensorMap& tmap_k,
+                                    const CUtensorMap& tmap_v, const PrefillItem* items, const int4* units,
+                                    int n_units, const int4* comb, int n_comb, const int32_t* tables,
+                                    __nv_bfloat16* out, float* part_o, float* part_ml, const AttnShape& s,
+                                    cudaStream_t stream) {
+    if (n_units <= 0) return cudaSuccess;
+    auto run = [&](auto hd_tag) -> cudaError_t {
+        constexpr int HD = decltype(hd_tag)::value;
+        using C = PCfg<HD>;
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(prefill_attention_kernel<HD>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        cudaError_t e = launch_k(prefill_attention_kernel<HD>, dim3(n_units, s.hkv, 1), dim3(kPThreads), C::kSmem,
+                                 stream, tmap_q, tmap_k, tmap_v, items, tables, out, part_o, part_ml, units, 0, s);
+        if (e == cudaSuccess && n_comb > 0)
+            e = launch_k(prefill_combine_units_kernel<HD>, dim3(n_comb, s.hkv, 256 / 8), dim3(HD, 8), 0, stream, items, comb,
+                         static_cast<const float*>(part_o), static_cast<const float*>(part_ml), out, s.hq, s.hkv);
+        return e;
+    };
+    if (s.hd == 128) return run(std::integral_constant<int, 128>{});
+    if (s.hd == 64) return run(std::integral_constant<int, 64>{});
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t prefill_attention(const CUtensorMap& tmap_q, const CUtensorMap& tmap_k,

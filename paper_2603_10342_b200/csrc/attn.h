@@ -1,4 +1,5 @@
 #pragma once
+#include <vector>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -45,6 +46,16 @@ struct AttnShape {
 int prefill_tokens_per_tile(int hq, int hkv);
 int prefill_tokens_per_cta(int hq, int hkv);
 int prefill_splits(int n_items, int hkv, int max_blocks, int num_sms, size_t ws_rows);
+// Work-unit form (one wave; only items longer than the per-CTA page budget split).  units[u] =
+// (item, first page, pages, partial slot or -1); comb[c] = (item, first slot, slots).
+// prefill_units returns 0 when the uniform path should be used instead.
+int prefill_units(const PrefillItem* items, int n_items, int hkv, int num_sms, size_t ws_rows,
+                  std::vector<int4>& units, std::vector<int4>& comb);
+cudaError_t prefill_attention_units(const CUtensorMap& tmap_q, const CUtensorMap& tmap_k,
+                                    const CUtensorMap& tmap_v, const PrefillItem* items, const int4* units,
+                                    int n_units, const int4* comb, int n_comb, const int32_t* tables,
+                                    __nv_bfloat16* out, float* part_o, float* part_ml, const AttnShape& s,
+                                    cudaStream_t stream);
 cudaError_t prefill_attention(const CUtensorMap& tmap_q, const CUtensorMap& tmap_k,
                               const CUtensorMap& tmap_v, const PrefillItem* items, int n_items,
                               int max_blocks, int splits, const int32_t* tables,

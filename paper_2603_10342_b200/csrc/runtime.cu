@@ -883,7 +883,8 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->ppart_o = static_cast<float*>(dmalloc(L->ppart_rows * s.hd * 4, L->allocs));
         L->ppart_ml = static_cast<float*>(dmalloc(L->ppart_rows * 2 * 4, L->allocs));
         L->meta_ints = size_t(3) * T + L->max_segs + L->max_tbl + 4 * size_t(L->max_segs) +
-                       4 * size_t(L->max_pitems) + 64;
+                       4 * size_t(L->max_pitems) + 64 +
+                       4 * (size_t(L->max_pitems) + 512) + 4;  // prefill work units + combine list
         L->d_meta = static_cast<int32_t*>(dmalloc(L->meta_ints * 4, L->allocs));
         cuda_check(cudaMallocHost(&L->h_meta, L->meta_ints * 4), "cudaMallocHost");
         L->d_out = static_cast<unsigned long long*>(dmalloc(size_t(L->max_segs) * 8, L->allocs));
@@ -1005,7 +1006,16 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         std::memcpy(h_ditems, ditems.data(), ditems.size() * sizeof(DecodeItem));
         int32_t* h_pitems = h_ditems + 4 * L->max_segs;
         std::memcpy(h_pitems, pitems.data(), pitems.size() * sizeof(PrefillItem));
-        const size_t used = size_t(h_pitems - hm) + 4 * pitems.size();
+        // prefill work units (one wave, long causal items split; ASB_PREFILL_UNITS=0 off), int4-aligned
+        static const bool units_off = std::getenv("ASB_PREFILL_UNITS") && std::atoi(std::getenv("ASB_PREFILL_UNITS")) == 0;
+        static const bool psplit_forced = std::getenv("ASB_PREFILL_SPLITS") != nullptr;
+        std::vector<int4> punits, pcomb;
+        if (!units_off && !psplit_forced && !pitems.empty())
+            prefill_units(pitems.data(), int(pitems.size()), s.hkv, L->n_sms(), L->ppart_rows, punits, pcomb);
+        const size_t units_off_ints = (size_t(h_pitems - hm) + 4 * pitems.size() + 3) & ~size_t(3);
+        std::memcpy(hm + units_off_ints, punits.data(), punits.size() * sizeof(int4));
+        std::memcpy(hm + units_off_ints + 4 * punits.size(), pcomb.data(), pcomb.size() * sizeof(int4));
+        const size_t used = units_off_ints + 4 * (punits.size() + pcomb.size());
 
         cudaStream_t st = L->stream;
         cuda_check(cudaEventRecord(L->ev0, st), "event");
@@ -1019,6 +1029,8 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         const DecodeItem* d_ditems = reinterpret_cast<const DecodeItem*>(d_tbl + L->max_tbl);
         const PrefillItem* d_pitems =
             reinterpret_cast<const PrefillItem*>(d_tbl + L->max_tbl + 4 * L->max_segs);
+        const int4* d_units = reinterpret_cast<const int4*>(L->d_meta + units_off_ints);
+        const int4* d_comb = d_units + punits.size();
 
         // ---- forward -----------------------------------------------------------------------
         const int qd = s.hq * s.hd, kvd = s.hkv * s.hd;
@@ -1147,7 +1159,9 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
             // prefill attention (+ its split combine); final norm and argmax when not fused
             L->n_launch += 1 + int64_t(s.layers - 1) * ((dg_qkv || post_attn) ? 0 : 1) +
                            int64_t(s.layers) * ((dg_gu || post_mlp ? 0 : 1) + (fuse_qkv ? 0 : 1) +
-                                                (ditems.empty() ? 0 : 1) + (pitems.empty() ? 0 : (psplits > 1 ? 2 : 1)));
+                                                (ditems.empty() ? 0 : 1) + (pitems.empty() ? 0
+                                                 : !punits.empty() ? (pcomb.empty() ? 1 : 2)
+                                                                   : (psplits > 1 ? 2 : 1)));
             if (n_logit > 0 && !dg_lm) L->n_launch += (post_final ? 0 : 1) + (n_logit <= 256 ? 0 : 1);
             PostNorm pn_attn{}, pn_mlp{}, pn_final{};
             if (post_mlp || post_attn || post_final) {
@@ -1188,10 +1202,16 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                     });
                 if (!pitems.empty())
                     L->timed(ASB_STAT_PREFILL_ATTN, pattn_flops, [&] {
-                        cuda_check(prefill_attention(L->map_q, kv->tk, kv->tv, d_pitems, int(pitems.size()),
-                                                     max_pblocks, psplits, d_tbl, L->attn, L->ppart_o,
-                                                     L->ppart_ml, as, st),
-                                   "prefill attention");
+                        if (!punits.empty())
+                            cuda_check(prefill_attention_units(L->map_q, kv->tk, kv->tv, d_pitems, d_units,
+                                                               int(punits.size()), d_comb, int(pcomb.size()), d_tbl,
+                                                               L->attn, L->ppart_o, L->ppart_ml, as, st),
+                                       "prefill attention (units)");
+                        else
+                            cuda_check(prefill_attention(L->map_q, kv->tk, kv->tv, d_pitems, int(pitems.size()),
+                                                         max_pblocks, psplits, d_tbl, L->attn, L->ppart_o,
+                                                         L->ppart_ml, as, st),
+                                       "prefill attention");
                     });
                 pn_mlp.w = post_mlp ? ly.mlp_norm : nullptr;
                 if (!skip("o"))
