@@ -1,90 +1,48 @@
 #!/usr/bin/env python3
 """AgentServe hot-path benchmark on B200 (driver contract: one JSON line on rank 0).
 
-A *step* is one full serving episode of BASELINE.json configs[1] (C2): a Qwen2.5-0.5B-shaped
-random-init SLM serving 8 concurrent ReAct agents per GPU (2048-token system prompt, four
-256-token tool outputs, 8-64-token decodes, 100 ms tool latency, 500 ms arrival stagger),
-scheduled by the AgentServe policy (TPOT controller + resume budget + Green Context
-partitions) and executed for real on the B200 through the drop-in agsv_* C ABI.
+A *step* is one full serving episode of a BASELINE.json configuration (default C3, the
+north_star target: a Llama-3.2-3B-shaped random-init SLM serving 32 concurrent ReAct agents per
+GPU, mixed cold/resume/decode arrivals), scheduled by the AgentServe policy (TPOT controller +
+resume-prefill budget + Green Context partitions) and executed for real on the B200 through
+the drop-in agsv_* C ABI.  The same episodes are then served by the unpartitioned FCFS policy
+(`mixed_fcfs`, the llama.cpp archetype) on the same kernels, and both are reported in the line.
 
-metric  : served decode tokens / s (the reference's throughput_tps, metrics.cpp:144-155)
-          whole job over all GPUs; p50/p95/p99 TTFT and TPOT reported alongside.
-value   : emitted tokens / summed episode time on the engine's clock (device completions).
+metric  : served decode tokens / s (the reference's throughput_tps, metrics.cpp:144-155),
+          whole job over all GPUs; p50/p95/p99 TTFT and TPOT (the reference's definitions,
+          metrics.cpp:71-92, pooled over all timed episodes) for both policies.
+value   : AgentServe emitted tokens / episode time on the engine's clock (device completions),
+          slowest rank.
 e2e     : the same tokens / wall time around the agsv_simulate C-ABI call from this host
-          client (config JSON in, trace out; token ids H2D and greedy ids D2H every step).
+          client (config JSON in, trace out; token ids and block tables H2D and greedy ids D2H
+          every forward, counted by the lanes).
 roofline: dominant kernel category by device time, timed with CUDA events on the lane stream
           (backend.profile_kernels) during one profiled replay of the same episode right after
-          the timed ones, against MEASURED_PEAKS.json.  Per-launch events serialise the
-          programmatic-dependent-launch overlap, so the timed episodes run without them.
+          the timed ones, against MEASURED_PEAKS.json; `traffic` from the committed ncu capture
+          of the same config (profiles/ncu_traffic_<config>.json, scripts/ncu_traffic.py).
 cpu_baseline / --impl reference: the CPU fp32 oracle forward (oracle/forward.c) on the box's
-          host cores, sampled and extrapolated to the same episode (see _cpu_baseline).
+          host cores executing a real slice of the same episode (see cpu_slice).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl mine|reference]
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-AGENTS_PER_GPU = 8
-MODEL = "qwen2.5-0.5b"
+from paper_2603_10342_b200 import workloads  # noqa: E402
+
 METRIC = "served decode tokens/s per GPU under the agent trace (p50/p99 TTFT & TPOT ms; decode-attn HBM GB/s)"
-
-# B200 slot grid: 9 levels of 16 SMs (Green Context splits are multiples of 8 on sm_100);
-# throughput curves shaped from the kernel probes (decode saturates early, cold prefill late).
-B200_PROFILE_SHAPE = {"total_sms": 144, "granularity": 16, "decode_max_rate": 4000.0,
-                      "decode_knee": 0.3, "cold_max_rate": 280000.0, "cold_knee": 0.9,
-                      "resume_max_rate": 120000.0, "resume_knee": 0.5}
-
-
-def profile_doc(api) -> tuple[str, str]:
-    """ProfileBundle for the controller: the B200 curves measured with our kernels on Green
-    Context partitions (paper_2603_10342_b200.profile_measure, committed under profiles/) when
-    present, else the hand-shaped fallback.  Returns (json text, source)."""
-    path = ROOT / "profiles" / f"b200_profile_{MODEL}.json"
-    if path.exists():
-        doc = json.loads(path.read_text())
-        doc.pop("measured", None)
-        return json.dumps(doc), f"measured ({path.relative_to(ROOT)})"
-    text, _ = api.profile_generate(B200_PROFILE_SHAPE)
-    return text, "shaped (B200_PROFILE_SHAPE)"
-
-
-def workload_config(n_gpus: int, rank: int, clock: str = "wall", policy: str = "agentserve",
-                    profile_doc: str | None = None, profile_kernels: bool = False) -> dict:
-    cfg = {
-        "workload": {"paradigm": "react", "model": "qwen2.5-3b", "concurrency": AGENTS_PER_GPU * n_gpus,
-                     "stagger_ms": 500.0, "steps_per_session": 4,
-                     "cold": {"min": 2048, "max": 2048, "mean": 2048},
-                     "resume": {"min": 256, "max": 256, "mean": 256},
-                     "decode": {"min": 8, "max": 64, "mean": 32},
-                     "tool_delay": {"kind": "fixed", "ms": 100.0}},
-        # SLO calibrated from the profile as the reference does when no thresholds are given
-        # (calibrate_slo, factor 8: src/metrics.cpp:30-43, src/config.cpp); with the measured
-        # B200 profile this lets the adaptive controller grow the decode partition
-        "slo": {"factor": 8.0, "tpot_stat": "p95"},
-        "policy": policy,
-        "seed": 13,
-    }
-    if profile_doc:
-        cfg["profile"] = {"inline": json.loads(profile_doc)}
-    if n_gpus > 1:
-        cfg["workload"]["shard_index"] = rank
-        cfg["workload"]["shard_count"] = n_gpus
-    if clock != "virtual":
-        cfg["backend"] = {"clock": clock, "model": MODEL, "device": 0, "profile_kernels": profile_kernels,
-                          "prefill_unit_tokens": 2048}
-    return cfg
 
 
 def _peaks() -> dict:
@@ -146,72 +104,163 @@ class ClockSampler:
                 "samples": len(sms)}
 
 
-def _episode_stats(recs: list[dict]) -> dict:
+def pct(xs: list[float], p: float) -> float | None:
+    """nearest-rank percentile (metrics.cpp:45-59)"""
+    if not xs:
+        return None
+    s = sorted(xs)
+    k = max(1, math.ceil(p / 100.0 * len(s)))
+    return s[min(k, len(s)) - 1]
+
+
+def episode_stats(recs: list[dict], metrics: dict) -> dict:
+    """Counts, per-gap TPOT samples and TTFTs of one episode trace (the reference's
+    collect_tokens walk, metrics.cpp:71-92: gap chains break at decode-phase starts)."""
     foot = recs[-1]
-    dev = foot.get("device", {})
     steps = [r for r in recs if r.get("k") == "step_done"]
-    tokens = sum(len(s["emit"]) for s in steps)
-    return {"tokens": tokens, "end_ms": foot["end_ms"], "device": dev,
-            "n_steps": len(steps),
-            "prefill_tokens": sum(r["len"] for r in recs if r.get("k") == "prefill_done" and r.get("ctx") != "decode"),
-            "chunk_tokens": sum(s.get("chunk", 0) for s in steps),
-            "batch_sizes": [s["batch"] for s in steps],
+    gaps, prev = [], {}
+    for r in recs:
+        if r.get("k") == "issue" and r.get("req") == "decode":
+            prev[r["s"]] = None
+        elif r.get("k") == "step_done":
+            for s in r["emit"]:
+                if prev.get(s) is not None:
+                    gaps.append(r["t"] - prev[s])
+                prev[s] = r["t"]
+    return {"tokens": sum(len(s["emit"]) for s in steps), "end_ms": foot["end_ms"],
+            "device": foot.get("device", {}), "n_steps": len(steps),
+            "gaps": gaps, "ttft": [s["ttft_ms"] for s in metrics["sessions"] if s["ttft_ms"] >= 0],
+            "slo": metrics.get("slo_attainment", metrics.get("joint_slo_attainment")),
             "step_sms": [(s.get("sms", 0), s.get("dev_ms", 0.0)) for s in steps]}
 
 
-_ORACLE = {}
+# ------------------------------------------------------------------------------- CPU baseline
+class CpuSlice:
+    """The CPU fp32 oracle (oracle/forward.c, OpenMP over all host cores) serving a REAL slice
+    of the same episode: the trace's Q_P prefills (cold prompts, resumes over budget) and
+    decode steps (every stream's row + the admitted-resume chunk) are executed in trace order
+    with the config's full-width model truncated to 2 and to 1 decoder layers (same events
+    on both), for a wall-time budget.  Per-forward and per-layer costs separate from the two
+    runs: full-depth cost = base + L * per_layer, with base = 2*T1 - T2 and per_layer =
+    T2 - T1 over the same events.  The episode estimate prices the unexecuted rest of the
+    trace at the slice's measured per-token (prefill) and per-row (decode) rates.  State
+    persists across calls, so repeated steps extend one slice."""
+
+    def __init__(self, cfg_name: str, recs: list[dict], seed: int = 13):
+        from oracle.forward import OracleModel, PRESETS
+        self.cfg_name = cfg_name
+        self.model = workloads.CONFIGS[cfg_name]["model"]
+        self.layers = PRESETS[self.model]["layers"]
+        self.seed = seed
+        self.recs = recs
+        self.work = self._work_items(recs)
+        tot = {}  # tokens each session accumulates over the episode -> the oracle's KV capacity
+        for kind, s, n, _, r in self.work:
+            if kind == "prefill":
+                tot[s] = tot.get(s, 0) + n
+                continue
+            for e in r["emit"]:
+                tot[e] = tot.get(e, 0) + 1
+            if r.get("chunk"):
+                tot[r["chunk_s"]] = tot.get(r["chunk_s"], 0) + int(r["chunk"])
+        max_ctx = max(tot.values(), default=0)
+        self.m2 = OracleModel(self.model, seed=seed, max_ctx=max_ctx + 64, layers_limit=min(2, self.layers))
+        self.m1 = OracleModel(self.model, seed=seed, max_ctx=max_ctx + 64, layers_limit=1)
+        self.s2, self.s1 = {}, {}
+        self.done = 0  # work items executed
+        self.t2 = {"prefill": 0.0, "step": 0.0}
+        self.t1 = {"prefill": 0.0, "step": 0.0}
+        self.cnt = {"prefill_tokens": 0, "step_rows": 0, "steps": 0}
+
+    @staticmethod
+    def _work_items(recs):
+        """(kind, session, tokens, rows, record) in trace order: 'prefill' = one Q_P job (cold
+        prompt or resume over budget); 'step' = one decode step (rows = its single-token
+        streams, tokens = rows + the admitted-resume chunk)."""
+        out = []
+        for r in recs:
+            k = r.get("k")
+            if k == "prefill_done" and r.get("ctx") != "decode":
+                out.append(("prefill", r["s"], int(r["len"]), 0, r))
+            elif k == "step_done":
+                rows = len(r["emit"])
+                out.append(("step", -1, rows + int(r.get("chunk", 0)), rows, r))
+        return out
+
+    def _exec(self, model, sess, item):
+        import numpy as np
+        kind, s, n, rows, r = item
+        V = model.spec.vocab
+        if kind == "prefill":
+            ss = sess.setdefault(s, model.session())
+            ss.forward(np.random.default_rng(s).integers(0, V, n, dtype=np.int32))
+            return
+        for e in r["emit"]:
+            sess.setdefault(e, model.session()).forward(np.array([1 + e % (V - 1)], dtype=np.int32))
+        chunk = int(r.get("chunk", 0))
+        if chunk > 0:
+            cs = r["chunk_s"]
+            sess.setdefault(cs, model.session()).forward(
+                np.random.default_rng(cs).integers(0, V, chunk, dtype=np.int32))
+
+    def run(self, budget_s: float) -> None:
+        t_end = time.perf_counter() + budget_s
+        while self.done < len(self.work) and time.perf_counter() < t_end:
+            item = self.work[self.done]
+            t0 = time.perf_counter()
+            self._exec(self.m2, self.s2, item)
+            t1 = time.perf_counter()
+            self._exec(self.m1, self.s1, item)
+            t2 = time.perf_counter()
+            self.t2[item[0]] += t1 - t0
+            self.t1[item[0]] += t2 - t1
+            if item[0] == "prefill":
+                self.cnt["prefill_tokens"] += item[2]
+            else:
+                self.cnt["step_rows"] += item[2]
+                self.cnt["steps"] += 1
+            self.done += 1
+
+    def estimate(self) -> dict:
+        L = self.layers
+
+        def full(kind):
+            t2, t1 = self.t2[kind], self.t1[kind]
+            per_layer = max(t2 - t1, 0.0)
+            base = max(t1 - per_layer, 0.0)
+            return base + L * per_layer
+
+        t_pf, t_st = full("prefill"), full("step")
+        rest_pf = sum(w[2] for w in self.work[self.done:] if w[0] == "prefill")
+        rest_rows = sum(w[2] for w in self.work[self.done:] if w[0] == "step")
+        rate_pf = t_pf / self.cnt["prefill_tokens"] if self.cnt["prefill_tokens"] else None
+        rate_row = t_st / self.cnt["step_rows"] if self.cnt["step_rows"] else None
+        if rate_row is None and rate_pf is not None:
+            rate_row = rate_pf  # a decode row costs at least a prefill token
+        if rate_pf is None and rate_row is not None:
+            rate_pf = rate_row
+        t_total = t_pf + t_st + (rest_pf * rate_pf if rate_pf else 0.0) + (rest_rows * rate_row if rate_row else 0.0)
+        tokens = sum(len(r["emit"]) for r in self.recs if r.get("k") == "step_done")
+        return {"value": tokens / t_total if t_total > 0 else 0.0, "unit": "tokens/s",
+                "cores": os.cpu_count(), "kind": "port",
+                "sample": (f"CPU fp32 oracle (oracle/forward.c, OpenMP {os.cpu_count()} threads) executed the first "
+                           f"{self.done} of {len(self.work)} work items of the {self.cfg_name.upper()} episode trace in "
+                           f"order ({self.cnt['prefill_tokens']} Q_P prefill tokens, {self.cnt['steps']} decode steps / "
+                           f"{self.cnt['step_rows']} rows) on the full-width {self.model} truncated to 2 and 1 of {L} "
+                           f"layers; full depth = base + {L} x per-layer cost; the rest of the episode "
+                           f"({rest_pf} prefill tokens, {rest_rows} step rows) priced at the slice's measured rates; "
+                           f"episode estimate {t_total:.1f} s for {tokens} tokens")}
 
 
-def _cpu_baseline(tmpl_stats: dict, budget_s: float = 20.0) -> dict:
-    """CPU fp32 oracle forward on the host cores, on a bounded sample of the same workload:
-    one 128-token prefill and a few 8-row decode steps (8 sessions x 1 token on short
-    contexts) timed with all OpenMP threads, then extrapolated to the episode's measured work
-    (prefill tokens and decode steps counted from the episode's trace).  The short sampled
-    contexts under-count CPU attention work, so this is an upper bound on CPU throughput."""
-    import numpy as np
-    from oracle.forward import OracleModel, token_stream
-    t0 = time.perf_counter()
-    if MODEL not in _ORACLE:
-        _ORACLE[MODEL] = OracleModel(MODEL, seed=13, max_ctx=512)
-    om = _ORACLE[MODEL]
-    build_s = time.perf_counter() - t0
-    V = om.spec.vocab
-    sess = [om.session() for _ in range(AGENTS_PER_GPU)]
-    n_pf = 128
-    t0 = time.perf_counter()
-    sess[0].forward(token_stream(13, "tok/0/cold", n_pf, V))
-    prefill_s = time.perf_counter() - t0
-    for i in range(1, AGENTS_PER_GPU):
-        sess[i].forward(token_stream(13, f"tok/{i}/cold", 32, V))
-    steps, step_s = 0, 0.0
-    deadline = time.perf_counter() + budget_s
-    while steps < 2 and time.perf_counter() < deadline:
-        t0 = time.perf_counter()
-        for s in sess:
-            s.forward(np.array([1 + steps], dtype=np.int32))
-        step_s += time.perf_counter() - t0
-        steps += 1
-    per_step = step_s / max(steps, 1)  # 8 rows
-    per_prefill_tok = prefill_s / float(n_pf)
-    ep = tmpl_stats
-    t_cpu = (ep["prefill_tokens"] + ep["chunk_tokens"]) * per_prefill_tok + \
-        ep["n_steps"] * per_step * (np.mean(ep["batch_sizes"]) / AGENTS_PER_GPU if ep["batch_sizes"] else 1.0)
-    return {"value": ep["tokens"] / t_cpu if t_cpu > 0 else 0.0, "unit": "tokens/s",
-            "cores": os.cpu_count(), "kind": "port",
-            "sample": (f"CPU fp32 oracle ({MODEL}, OpenMP {os.cpu_count()} threads): {n_pf}-token prefill "
-                       f"{prefill_s:.2f}s, {steps} decode steps x {AGENTS_PER_GPU} rows @ctx <=130 "
-                       f"{per_step:.2f}s/step (weights built in {build_s:.1f}s); extrapolated to the "
-                       f"episode's {ep['prefill_tokens'] + ep['chunk_tokens']} prefill tokens and "
-                       f"{ep['n_steps']} decode steps")}
-
-
+# ------------------------------------------------------------------------------- harness
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws <= 1:
         return 1, 0, None
     import torch.distributed as dist
-    backend = "nccl" if os.environ.get("BENCH_BACKEND", "nccl") == "nccl" else "gloo"
-    dist.init_process_group(backend=backend)
+    # sessions never exchange data: the harness's barrier / max / gather are host plumbing,
+    # kept off NCCL by default (north_star: no NCCL)
+    dist.init_process_group(backend=os.environ.get("BENCH_BACKEND", "gloo"))
     return ws, dist.get_rank(), dist
 
 
@@ -225,21 +274,12 @@ def _reduce(dist, vals: list[float], op: str) -> list[float]:
     return t.cpu().tolist()
 
 
-def _gather_lat(dist, xs: list[float]) -> list[float]:
+def _gather(dist, xs: list) -> list:
     if dist is None:
         return xs
     out = [None] * dist.get_world_size()
     dist.all_gather_object(out, xs)
     return [v for part in out for v in part]
-
-
-def _pct(xs: list[float], p: float) -> float | None:
-    import math
-    if not xs:
-        return None
-    s = sorted(xs)
-    k = max(1, math.ceil(p / 100.0 * len(s)))
-    return s[min(k, len(s)) - 1]
 
 
 def device_index() -> tuple[int, int]:
@@ -255,33 +295,43 @@ def device_index() -> tuple[int, int]:
     return local, local
 
 
+def policy_summary(stats: list[dict], dist, tokens_all: float, t_max_ms: float) -> dict:
+    gaps = _gather(dist, [g for s in stats for g in s["gaps"]])
+    ttft = _gather(dist, [t for s in stats for t in s["ttft"]])
+    slo = _gather(dist, [s["slo"] for s in stats if s["slo"] is not None])
+    return {"tokens_per_s": round(tokens_all / (t_max_ms / 1000.0), 2) if t_max_ms > 0 else 0.0,
+            "ttft_ms": {f"p{p}": round(pct(ttft, p), 3) if ttft else None for p in (50, 95, 99)},
+            "tpot_ms": {f"p{p}": round(pct(gaps, p), 3) if gaps else None for p in (50, 95, 99)},
+            "slo_attainment": round(sum(slo) / len(slo), 4) if slo else None,
+            "sessions": len(ttft), "tpot_gaps": len(gaps)}
+
+
 def run_mine(args) -> None:
     n_gpus, rank, dist = _dist()
     import torch
     dev_idx, phys_idx = device_index()
-    if args.virtual:
-        clock = "virtual"
-    else:
-        clock = "wall"
+    clock = "virtual" if args.virtual else "wall"
+    if clock == "wall":
         torch.cuda.set_device(dev_idx)
     from paper_2603_10342_b200.agsv import Agsv
     api = Agsv()
-    prof_doc, prof_src = profile_doc(api)
-    cfg = workload_config(n_gpus, rank, clock, args.policy, prof_doc)
-    if clock == "wall":
-        cfg["backend"]["device"] = dev_idx
+
+    def cfg_of(policy, profile_kernels=False):
+        return workloads.run_config(args.config, clock=clock, policy=policy, n_shards=n_gpus, shard=rank,
+                                    device=dev_idx, profile_kernels=profile_kernels)
+
+    cfg = cfg_of(args.policy)
     td = tempfile.mkdtemp()
 
-    def episode(c=cfg):
+    def episode(c):
         t0 = time.perf_counter()
         tr = api.run(c)
         recs = [json.loads(x) for x in tr.jsonl(td).splitlines()]
         m = tr.metrics()
-        wall = time.perf_counter() - t0
-        return recs, m, wall
+        return recs, m, time.perf_counter() - t0
 
     for _ in range(args.warmup):
-        episode()
+        episode(cfg)
     if dist is not None:
         dist.barrier()
     if clock == "wall":
@@ -291,7 +341,7 @@ def run_mine(args) -> None:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
     t_wall0 = time.perf_counter()
-    eps = [episode() for _ in range(args.steps)]
+    eps = [episode(cfg) for _ in range(args.steps)]
     t_wall = time.perf_counter() - t_wall0
     if clock == "wall":
         ev1.record()
@@ -299,96 +349,100 @@ def run_mine(args) -> None:
         span_ms = ev0.elapsed_time(ev1)
         clocks = sampler.stop()
     else:
-        span_ms = t_wall * 1000.0
-        clocks = None
+        span_ms, clocks = t_wall * 1000.0, None
     if dist is not None:
         dist.barrier()
+    stats = [episode_stats(r, m) for r, m, _ in eps]
+
+    # the unpartitioned FCFS arm on the same kernels and the same episodes
+    cmp_stats = []
+    if args.compare != "none":
+        ccfg = cfg_of(args.compare)
+        episode(ccfg)  # warm
+        cmp_stats = [episode_stats(r, m) for r, m, _ in (episode(ccfg) for _ in range(max(1, args.steps)))]
+
     # profiled replay (per-launch CUDA events) for the kernel breakdown / roofline
     prof_stats = None
     if clock == "wall":
-        pcfg = json.loads(json.dumps(cfg))
-        pcfg["backend"]["profile_kernels"] = True
-        prof_stats = _episode_stats(episode(pcfg)[0])
+        r, m, _ = episode(cfg_of(args.policy, profile_kernels=True))
+        prof_stats = episode_stats(r, m)
 
-    stats = [_episode_stats(r) for r, _, _ in eps]
     tokens = sum(s["tokens"] for s in stats)
     engine_ms = sum(s["end_ms"] for s in stats)
     e2e_s = sum(w for _, _, w in eps)
-    ttft = [s["ttft_ms"] for _, m, _ in eps for s in m["sessions"] if s["ttft_ms"] >= 0]
-    gaps_p = {k: [m[k] for _, m, _ in eps] for k in ("tpot_p50_ms", "tpot_p95_ms", "tpot_p99_ms")}
-    # per-gap TPOT across all sessions of all episodes, from the traces
-    tpot = []
-    for recs, _, _ in eps:
-        prev = {}
-        for r in recs:
-            if r.get("k") == "issue" and r.get("req") == "decode":
-                prev[r["s"]] = None
-            elif r.get("k") == "step_done":
-                for s in r["emit"]:
-                    if prev.get(s) is not None:
-                        tpot.append(r["t"] - prev[s])
-                    prev[s] = r["t"]
-    # kernel categories (device time from CUDA events inside the lanes)
-    cats = {}
     io = {"kernel_launches": 0, "h2d_bytes": 0, "d2h_bytes": 0}
     for s in stats:
         for kk in io:
             io[kk] += s["device"].get("io", {}).get(kk, 0)
-    for s in ([prof_stats] if prof_stats else []):
-        k = s["device"].get("kernels", {})
-        for name, lanes in k.items():
+    cats = {}
+    if prof_stats:
+        for name, lanes in prof_stats["device"].get("kernels", {}).items():
             c = cats.setdefault(name, {"ms": 0.0, "units": 0.0, "launches": 0, "unit": lanes.get("unit")})
             for ln in ("decode_lane", "prefill_lane"):
                 if ln in lanes:
                     c["ms"] += lanes[ln]["ms"]
                     c["units"] += lanes[ln]["units"]
                     c["launches"] += lanes[ln]["launches"]
-
-    red = _reduce(dist, [float(tokens), float(engine_ms), float(e2e_s), float(span_ms)], "sum")
-    mx = _reduce(dist, [float(engine_ms), float(e2e_s), float(span_ms)], "max")
-    tokens_all = red[0]
-    ttft_all = _gather_lat(dist, ttft)
-    tpot_all = _gather_lat(dist, tpot)
+    c_tokens = sum(s["tokens"] for s in cmp_stats)
+    c_ms = sum(s["end_ms"] for s in cmp_stats)
+    red = _reduce(dist, [float(tokens), float(c_tokens)], "sum")
+    mx = _reduce(dist, [float(engine_ms), float(e2e_s), float(span_ms), float(c_ms)], "max")
+    main_sum = policy_summary(stats, dist, red[0], mx[0])
+    cmp_sum = policy_summary(cmp_stats, dist, red[1], mx[3]) if cmp_stats else None
+    rebinds = _gather(dist, [s["device"].get("rebind_us", {}) for s in stats])
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
 
     peaks = _peaks()
-    value = tokens_all / (mx[0] / 1000.0) if mx[0] > 0 else 0.0  # whole job / slowest rank
-    e2e_value = tokens_all / mx[1] if mx[1] > 0 else 0.0
+    value = red[0] / (mx[0] / 1000.0) if mx[0] > 0 else 0.0  # whole job / slowest rank
+    e2e_value = red[0] / mx[1] if mx[1] > 0 else 0.0
+    label = workloads.CONFIGS[args.config]["label"]
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": n_gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mx[2] / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights from named splitmix64 sub-streams; synthetic token ids)",
-        "config": {"workload": f"C2: {MODEL}-shaped SLM, {AGENTS_PER_GPU} ReAct agents per GPU, 2048-token "
-                               "system prompt, 4x256-token tool outputs, 8-64-token decodes, 100 ms tools",
-                   "agents_per_gpu": AGENTS_PER_GPU, "policy": args.policy, "clock": clock,
+        "config": {"workload": label, "config": args.config.upper(),
+                   "model": workloads.CONFIGS[args.config]["model"],
+                   "agents_per_gpu": workloads.CONFIGS[args.config]["agents"], "policy": args.policy,
+                   "compare_policy": args.compare, "clock": clock,
                    "parallelism": f"session-sharded replicas x{n_gpus} (no collective)",
-                   "profile": prof_src,
-                   "l2": "weights (0.99 GB) and KV exceed the 126 MB L2; no flush needed"},
-        "latency_ms": {"ttft": {"p50": _pct(ttft_all, 50), "p95": _pct(ttft_all, 95), "p99": _pct(ttft_all, 99)},
-                       "tpot": {"p50": _pct(tpot_all, 50), "p95": _pct(tpot_all, 95), "p99": _pct(tpot_all, 99)},
-                       "sessions": len(ttft_all), "tpot_gaps": len(tpot_all)},
+                   "slo": cfg.get("slo"), "controller": cfg.get("controller"),
+                   "lend_idle_prefill": cfg.get("backend", {}).get("lend_idle_prefill"),
+                   "profile": str(workloads.profile_path(workloads.CONFIGS[args.config]["model"]).relative_to(ROOT)),
+                   "l2": "weights and KV exceed the 126 MB L2; no flush needed"},
+        "latency_ms": {"ttft": main_sum["ttft_ms"], "tpot": main_sum["tpot_ms"],
+                       "sessions": main_sum["sessions"], "tpot_gaps": main_sum["tpot_gaps"]},
+        "policies": {args.policy: main_sum, **({args.compare: cmp_sum} if cmp_sum else {})},
         "e2e": {"value": round(e2e_value, 3), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(io["h2d_bytes"] / max(1, args.steps)),
                 "d2h_bytes_per_step": int(io["d2h_bytes"] / max(1, args.steps))},
         "gpu_launches": int(io["kernel_launches"]),
     }
+    if cmp_sum:
+        def ratio(a, b):
+            return round(a / b, 4) if a is not None and b else None
+        line["tails_vs_" + args.compare] = {
+            f"{k}_{p}": ratio(main_sum[k + "_ms"][p], cmp_sum[k + "_ms"][p])
+            for k in ("ttft", "tpot") for p in ("p50", "p95", "p99")}
+    rb = [r for r in rebinds if r and r.get("n", 0) > 0]
+    if rb:
+        line["rebind_us"] = {"p50_max_over_episodes": max(r["p50"] for r in rb),
+                             "p99_max_over_episodes": max(r["p99"] for r in rb),
+                             "max": max(r["max"] for r in rb), "rebinds": sum(r["n"] for r in rb),
+                             "target": "< 50 us (PAPER.md:453)"}
     if clocks:
         line["clocks"] = clocks
-    # roofline: dominant category by device time (forward is the envelope, not a kernel)
     kern = {k: v for k, v in cats.items() if k != "forward" and v["ms"] > 0}
     if kern:
         dom_name, dom = max(kern.items(), key=lambda kv: kv[1]["ms"])
         hbm = dom["unit"] == "bytes"
         achieved = dom["units"] / (dom["ms"] / 1000.0) / (1e9 if hbm else 1e12)
         peak = peaks["hbm"] if hbm else peaks["bf16_sust"]
-        # DRAM bytes per launch of this category from an ncu capture of C2-shaped decode steps
-        # (scripts/ncu_traffic.py), and their ratio to the algorithmic bytes of the same launches
         traffic, traffic_ratio = None, None
-        tf = ROOT / "profiles" / "ncu_traffic.json"
+        tf = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
         if tf.exists():
             tdoc = json.loads(tf.read_text())
             traffic = tdoc.get(dom_name)
@@ -403,28 +457,24 @@ def run_mine(args) -> None:
                             "avg_launch_us": round(1000.0 * dom["ms"] / max(1, dom["launches"]), 2),
                             "share_of_device_time": round(dom["ms"] / sum(v["ms"] for v in kern.values()), 3),
                             "measured": "profiled replay of the timed episode (CUDA events per launch)"}
-        # context: the decode lane runs on a Green Context partition; a partition of n SMs can
-        # stream at most ~119 GB/s per SM with 32 KiB TMA requests (scripts/probes/stream.cu,
-        # profiles/r1_stream_probe_ldg.txt), so the attainable decode bandwidth is below HBM peak
         sms_w = [(n, ms) for s in stats for n, ms in s.get("step_sms", []) if n > 0 and ms > 0]
         if sms_w and hbm:
             mean_sms = sum(n * ms for n, ms in sms_w) / sum(ms for _, ms in sms_w)
-            ceil = min(peaks["hbm"], 119.0 * mean_sms)
             line["roofline"]["decode_sms_mean"] = round(mean_sms, 1)
-            line["roofline"]["partition_ceiling_gbs"] = round(ceil, 1)
-            line["roofline"]["frac_of_partition_ceiling"] = round(achieved / ceil, 4)
         da = cats.get("decode_attn")
         if da and da["ms"] > 0:
-            line["decode_attn"] = {"achieved_gbs": round(da["units"] / (da["ms"] / 1000.0) / 1e9, 1),
-                                   "frac_of_hbm": round(da["units"] / (da["ms"] / 1000.0) / 1e9 / peaks["hbm"], 4),
-                                   "launches": da["launches"]}
+            gbs = da["units"] / (da["ms"] / 1000.0) / 1e9
+            line["decode_attn"] = {"achieved_gbs": round(gbs, 1), "frac_of_hbm": round(gbs / peaks["hbm"], 4),
+                                   "launches": da["launches"],
+                                   "avg_launch_us": round(1000.0 * da["ms"] / max(1, da["launches"]), 2)}
         line["kernels"] = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
                                "achieved": round(v["units"] / (v["ms"] / 1000.0) / (1e9 if v["unit"] == "bytes" else 1e12), 2),
                                "unit": "GB/s" if v["unit"] == "bytes" else "TFLOP/s"}
                            for k, v in kern.items()}
-    if n_gpus == 1 and not args.no_cpu:
-        _cpu_baseline(stats[0], budget_s=5.0)  # warm the OpenMP pool and the weights' pages
-        line["cpu_baseline"] = _cpu_baseline(stats[0])
+    if n_gpus == 1 and not args.no_cpu and clock == "wall":
+        cs = CpuSlice(args.config, eps[0][0])
+        cs.run(args.cpu_budget)
+        line["cpu_baseline"] = cs.estimate()
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -432,9 +482,10 @@ def run_mine(args) -> None:
 
 def run_reference(args) -> None:
     """Reference arm: the reference has no forward, so its CPU implementation of
-    this path is the oracle port (oracle/forward.c), timed on the host cores on a bounded
-    sample of the same episode; the episode's work counts come from the reference
-    simulator (oracle/_ref/libagentsim.so) run on the same workload config."""
+    this path is the oracle port (oracle/forward.c) on the host cores, executing the same
+    episode: the trace of the config comes from the compiled reference simulator
+    (oracle/_ref/libagentsim.so, agsv_simulate) on the same workload config, and each bench
+    step extends one real slice of it (CpuSlice) by a bounded budget."""
     n, rank, dist = _dist()
     if rank != 0:
         if dist is not None:
@@ -443,28 +494,29 @@ def run_reference(args) -> None:
     from paper_2603_10342_b200.agsv import Agsv
     from tests.ref_oracle import REF_LIB
     api = Agsv(REF_LIB) if REF_LIB.exists() else Agsv()
-    prof_doc, prof_src = profile_doc(api)
-    cfg = workload_config(1, 0, "virtual", args.policy, prof_doc)
+    cfg = workloads.run_config(args.config, clock="virtual", policy=args.policy)
     td = tempfile.mkdtemp()
-    tr = api.run(cfg)
-    recs = [json.loads(x) for x in tr.jsonl(td).splitlines()]
-    st = _episode_stats(recs)
+    recs = [json.loads(x) for x in api.run(cfg).jsonl(td).splitlines()]
+    cs = CpuSlice(args.config, recs)
+    per_step = max(2.0, args.ref_budget / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
-        _cpu_baseline(st, budget_s=10.0)
-    vals = []
-    base = None
+        cs.run(per_step)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        base = _cpu_baseline(st, budget_s=10.0)
-        vals.append(base["value"])
+        cs.run(per_step)
     wall = time.perf_counter() - t0
-    v = sum(vals) / len(vals)
+    base = cs.estimate()
+    v = base["value"]
+    label = workloads.CONFIGS[args.config]["label"]
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s",
-            "n_gpus": n, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * wall / len(vals), 1),
+            "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1000 * wall / max(1, args.steps), 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": f"C2 episode ({MODEL}, {AGENTS_PER_GPU} agents) "
-                                                        "on the CPU fp32 oracle forward"},
-            "cpu_baseline": {**base, "value": round(v, 4)},
+            "data": "synthetic", "config": {"workload": label, "config": args.config.upper(),
+                                            "trace": "reference simulator (oracle/_ref/libagentsim.so), same workload config",
+                                            "policy": args.policy},
+            "cpu_baseline": {**base, "value": round(v, 4),
+                             "reference_simulator": "agsv_simulate of the compiled reference produced the episode trace"},
             "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -477,9 +529,13 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["mine", "reference"], default="mine")
+    ap.add_argument("--config", choices=sorted(workloads.CONFIGS), default="c3")
     ap.add_argument("--policy", default="agentserve")
+    ap.add_argument("--compare", default="mixed_fcfs", help="second policy on the same kernels ('none': skip)")
     ap.add_argument("--sim-clock", dest="virtual", action="store_true", help="virtual clock (CPU-only test mode)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU slice for cpu_baseline")
+    ap.add_argument("--ref-budget", type=float, default=150.0, help="reference arm: total CPU seconds over all steps")
     args = ap.parse_args()
     if args.warmup < 3 and not args.virtual:
         args.warmup = 3

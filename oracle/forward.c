@@ -265,16 +265,24 @@ static void rmsnorm_rows(const float* x, const float* w, float* y, int n, int d,
     }
 }
 
-/* y[r][o] = sum_k x[r][k] * W[o][k]  (fp32) */
+/* y[r][o] = sum_k x[r][k] * W[o][k]  (fp32 accumulation; the k-sum is vectorised, so its
+ * association order is the SIMD reduction's, not left-to-right -- a difference of a few fp32
+ * ulps, far below the bf16 rounding applied to every output).  Blocks of 16 weight rows stay
+ * in L2 while all activation rows stream past them. */
 static void matmul(const float* x, const float* W, float* y, int n, int k, int o) {
-#pragma omp parallel for schedule(static)
-    for (int j = 0; j < o; ++j) {
-        const float* wr = W + (size_t)j * k;
+    const int JB = 16;
+#pragma omp parallel for schedule(dynamic)
+    for (int jb = 0; jb < o; jb += JB) {
+        const int je = jb + JB < o ? jb + JB : o;
         for (int r = 0; r < n; ++r) {
             const float* xr = x + (size_t)r * k;
-            float acc = 0.f;
-            for (int i = 0; i < k; ++i) acc += xr[i] * wr[i];
-            y[(size_t)r * o + j] = acc;
+            for (int j = jb; j < je; ++j) {
+                const float* wr = W + (size_t)j * k;
+                float acc = 0.f;
+#pragma omp simd reduction(+ : acc)
+                for (int i = 0; i < k; ++i) acc += xr[i] * wr[i];
+                y[(size_t)r * o + j] = acc;
+            }
         }
     }
 }

@@ -23,7 +23,14 @@ CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "libagentserve_b200.so"
 INCLUDE = PKG.parent / "include"
+# nlohmann/json (header-only, MIT; 3.11.x) for the engine's config / trace documents.  Searched
+# in $NLOHMANN_JSON_INCLUDE (a directory holding nlohmann/json.hpp), then the system include
+# paths, then the copy this image ships inside cudnn_frontend.
 JSON_DIRS = [
+    *([Path(os.environ["NLOHMANN_JSON_INCLUDE"])] if os.environ.get("NLOHMANN_JSON_INCLUDE") else []),
+    Path("/usr/include"),
+    Path("/usr/local/include"),
+    Path(sys.prefix) / "include",
     Path("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty"),
 ]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -34,7 +41,9 @@ def _json_include() -> Path:
     for d in JSON_DIRS:
         if (d / "nlohmann" / "json.hpp").exists():
             return d / "nlohmann"
-    raise RuntimeError("nlohmann/json.hpp not found in the image")
+    raise RuntimeError("nlohmann/json.hpp (3.11.x) not found; install it (e.g. apt install "
+                       "nlohmann-json3-dev) or set NLOHMANN_JSON_INCLUDE to the directory that "
+                       "contains nlohmann/json.hpp. Searched: " + ", ".join(map(str, JSON_DIRS)))
 
 
 def _flags() -> list[str]:

@@ -477,15 +477,28 @@ cudaError_t launch_hd(const CUtensorMap& tk, const CUtensorMap& tv, const __nv_b
 }  // namespace
 
 int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits) {
-    // one wave at two resident CTAs per SM (a second partial wave and the split merge cost more
-    // than the imbalance of a ragged single wave: C3 73% -> 84%, C4 84% -> 92% of HBM peak),
-    // >= 2 sub-blocks per consumer warp
+    // Split-KV count minimising the makespan in waves of two resident CTAs per SM: a CTA of
+    // s splits does 1/s of an item's stream, so the cost is ceil(items*s / slots) / s, plus a
+    // small merge charge per extra split.  With items <= slots this is the one-wave rule
+    // (C3 73% -> 84%, C4 84% -> 92% of HBM peak on the full device); on a Green Context
+    // partition it also avoids ragged second waves (128 (row, head) items on a 48-SM
+    // partition: 1 split = 2 waves of full items, 3 splits = 4 waves of 1/3 items = 1.33).
+    // >= 2 sub-blocks per consumer warp.
     const int subs = (max_ctx + kSub - 1) / kSub;
-    const int base = n_items * hkv;
-    int splits = (2 * num_sms) / std::max(base, 1);
-    splits = std::min(splits, std::max(1, subs / (2 * kWarps)));
-    splits = std::min(splits, max_splits);
-    return std::max(splits, 1);
+    const int base = std::max(n_items * hkv, 1);
+    const int slots = 2 * std::max(num_sms, 1);
+    const int cap = std::max(1, std::min(max_splits, subs / (2 * kWarps)));
+    int best = 1;
+    double best_t = 1e30;
+    for (int sp = 1; sp <= cap; ++sp) {
+        const double waves = double((int64_t(base) * sp + slots - 1) / slots);
+        const double t = waves / sp * (1.0 + 0.03 * (sp - 1));
+        if (t < best_t - 1e-9) {
+            best_t = t;
+            best = sp;
+        }
+    }
+    return best;
 }
 
 cudaError_t decode_attention(const CUtensorMap& tmap_k32, const CUtensorMap& tmap_v32,

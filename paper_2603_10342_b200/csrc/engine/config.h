@@ -48,6 +48,10 @@ struct BackendCfg {
     int green_granularity = 0;      // SMs per slot on the device; 0: device_sms / total_slots
     bool emit_ids = true;           // record generated token ids in the trace
     bool profile_kernels = false;   // per-category kernel timing (CUDA events) in the footer
+    // Partitioned policies, wall clock: a decode step launched while Q_P holds no work runs on
+    // the full device instead of the decode partition (the idle prefill SMs are lent, and
+    // taken back at the next step once prefill work exists)
+    bool lend_idle_prefill = false;
     bool present = false;
     nlohmann::json to_json() const;
 };

@@ -2,6 +2,7 @@
 
 #include <cstdio>
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -104,6 +105,19 @@ DeviceExec::DeviceExec(const RunCfg& cfg, const std::vector<Plan>& plans) {
             if (!g_res || !g_res->busy) g_res = r;
         }
     }
+    // From here on the resident is marked busy: any throw before the constructor completes
+    // (the destructor does not run then) must hand it back, or it would stay pinned forever.
+    struct BusyGuard {
+        std::shared_ptr<Resident> r;
+        bool armed = true;
+        ~BusyGuard() {
+            if (!armed || !r) return;
+            if (r->dlane) asb_lane_wait(r->dlane);
+            if (r->plane) asb_lane_wait(r->plane);
+            std::lock_guard<std::mutex> lk(g_res_mu);
+            r->busy = false;
+        }
+    } guard{res_};
     model_ = res_->model;
     kv_ = res_->kv;
     dlane_ = res_->dlane;
@@ -150,6 +164,7 @@ DeviceExec::DeviceExec(const RunCfg& cfg, const std::vector<Plan>& plans) {
     info_["prefill_unit_tokens"] = unit_;
     info_["build"] = asb_build_info();
     start_clock();
+    guard.armed = false;
 }
 
 DeviceExec::~DeviceExec() {
@@ -233,16 +248,41 @@ int32_t DeviceExec::prefill_collect(float* dev_ms) {
     return id;
 }
 
-void DeviceExec::bind(int level, bool shared) {
-    if (!slots_) return;
+double DeviceExec::bind(int level, bool shared) {
+    if (!slots_) return 0.0;
+    const double t0 = now_ms();
     const int lvl = shared ? levels_ : level;
     void *sd = nullptr, *sp = nullptr;
     ok(asb_slots_bind(slots_, lvl, &sd, &sp), "asb_slots_bind");
-    ok(asb_lane_set_stream(dlane_, sd), "bind decode lane");
+    ok(asb_slots_sm_counts(slots_, lvl, &part_dsms_, &psms_), "sm counts");
+    level_ = lvl;
+    if (dfull_ && lvl != levels_) {
+        // keep borrowing the full device; the partition stream is taken at the next step
+        // that runs while prefill work exists (decode_on_full_device(false))
+    } else {
+        ok(asb_lane_set_stream(dlane_, sd), "bind decode lane");
+        dsms_ = part_dsms_;
+        ok(asb_lane_set_sms(dlane_, green() ? dsms_ : 0), "lane sms");
+    }
     ok(asb_lane_set_stream(plane_, sp), "bind prefill lane");
-    ok(asb_slots_sm_counts(slots_, lvl, &dsms_, &psms_), "sm counts");
-    ok(asb_lane_set_sms(dlane_, green() ? dsms_ : 0), "lane sms");
     ok(asb_lane_set_sms(plane_, green() ? psms_ : 0), "lane sms");
+    const double ms = now_ms() - t0;
+    rebind_us_.push_back(1000.0 * ms);
+    return ms;
+}
+
+void DeviceExec::decode_on_full_device(bool on) {
+    if (!slots_ || !green() || on == dfull_) return;
+    void* sd = nullptr;
+    const int lvl = on ? levels_ : level_;
+    ok(asb_slots_bind(slots_, lvl, &sd, nullptr), "asb_slots_bind");
+    int d = 0;
+    ok(asb_slots_sm_counts(slots_, lvl, &d, nullptr), "sm counts");
+    ok(asb_lane_set_stream(dlane_, sd), "lend decode lane");
+    dsms_ = d;
+    ok(asb_lane_set_sms(dlane_, lvl == levels_ ? 0 : dsms_), "lane sms");
+    dfull_ = on;
+    lend_switches_ += 1;
 }
 
 bool DeviceExec::green() const { return slots_ && asb_slots_green(slots_) == 1; }
@@ -299,6 +339,20 @@ json DeviceExec::describe() const {
     }
     j["green_contexts"] = green();
     j["levels"] = levels_;
+    {
+        // rebind latency (host cost of switching both lanes; non-blocking) vs the paper's
+        // < 50 us
+        std::vector<double> v = rebind_us_;
+        std::sort(v.begin(), v.end());
+        auto pct = [&](double p) {
+            if (v.empty()) return -1.0;
+            size_t k = static_cast<size_t>(std::ceil(p / 100.0 * double(v.size())));
+            k = std::max<size_t>(1, std::min(k, v.size()));
+            return v[k - 1];
+        };
+        j["rebind_us"] = {{"n", v.size()}, {"p50", pct(50)}, {"p99", pct(99)}, {"max", v.empty() ? -1.0 : v.back()}};
+        j["lend_switches"] = lend_switches_;
+    }
     if (slots_) {
         json lv = json::array();
         for (int l = 1; l <= levels_; ++l) {

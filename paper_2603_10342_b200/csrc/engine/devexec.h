@@ -54,7 +54,16 @@ public:
     int32_t prefill_collect(float* dev_ms);  // -1 when the unit produced no logits
 
     // ---- SM partitions
-    void bind(int decode_level, bool shared);
+    // Rebind both lanes to the (decode, prefill) streams of a slot level (shared = the
+    // full-device pair).  Non-blocking: in-flight work finishes on its old partition.
+    // Returns the measured host cost in ms.
+    double bind(int decode_level, bool shared);
+    // Work-conserving decode (backend.lend_idle_prefill): while the prefill partition has
+    // nothing to run, the decode lane borrows the full device; it returns to its partition
+    // at the next step once prefill work exists.  No-op without green contexts.
+    void decode_on_full_device(bool on);
+    bool decode_borrowing() const { return dfull_; }
+    void clear_rebind_stats() { rebind_us_.clear(); }
     bool green() const;
     int decode_sms() const { return dsms_; }
     int prefill_sms() const { return psms_; }
@@ -82,6 +91,10 @@ private:
     int levels_ = 0;
     std::vector<uint32_t> sessions_;
     int dsms_ = 0, psms_ = 0;
+    int level_ = 0, part_dsms_ = 0;  // current slot level and its decode partition size
+    bool dfull_ = false;
+    int64_t lend_switches_ = 0;
+    std::vector<double> rebind_us_;  // measured host cost of every rebind (non-blocking)
     int unit_ = 2048;
     int step_logit_rows_ = 0;
     bool prefill_want_ = false;

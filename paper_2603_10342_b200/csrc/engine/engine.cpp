@@ -152,7 +152,10 @@ private:
         ctrl_.r = c_.ctrl.r0;
         split_ = partition(c_.policy, c_.static_slots, ctrl_, c_.ctrl);
         if (mode_ == Mode::Partitioned) slots_.bind(split_.dslots, 0.0);  // initial, free
-        if (dev_ && clock_ == Clock::Wall) dev_->bind(slots_.decode_level(), split_.shared);
+        if (dev_ && clock_ == Clock::Wall) {
+            dev_->bind(slots_.decode_level(), split_.shared);
+            dev_->clear_rebind_stats();  // the initial binding is set-up, not a rebind
+        }
         acct_t0_ = 0.0;
         starved_since_ = 0.0;
         for (const auto& p : plans_) push(p.arrival, Kind::Arrival, p.id);
@@ -349,6 +352,8 @@ private:
         st.chunk_s = chunk_s;
         st.chunk = chunk;
         st.chunk_ms = chunk > 0 ? 1000.0 * chunk / prof_.mu_r(sms) : 0.0;
+        if (clock_ == Clock::Wall && mode_ == Mode::Partitioned && c_.backend.lend_idle_prefill)
+            dev_->decode_on_full_device(qp_.empty() && !span_);
         if (dev_) launch_step(st);
         if (clock_ == Clock::Wall) {
             st.start = now_;
@@ -696,11 +701,7 @@ private:
         if (mode_ == Mode::Partitioned && next.dslots != slots_.decode_level()) {
             if (auto rb = slots_.bind(next.dslots, t)) {
                 double oh = rb->oh;
-                if (clock_ == Clock::Wall) {
-                    const double b0 = dev_->now_ms();
-                    dev_->bind(next.dslots, false);
-                    oh = dev_->now_ms() - b0;  // measured switch cost
-                }
+                if (clock_ == Clock::Wall) oh = dev_->bind(next.dslots, false);  // measured switch cost
                 Event e = ev(Ev::Rebind, t);
                 e.from = rb->from;
                 e.to = rb->to;

@@ -114,7 +114,9 @@ __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_
     const uint4* wr = reinterpret_cast<const uint4*>(w);
     uint4* yr = reinterpret_cast<uint4*>(y + static_cast<size_t>(row) * d);
     const int nv = d / 8;
-    const float inv = rms_inv_warp(x + static_cast<size_t>(src_row) * d, d, eps, lane);
+    // 4 loads in flight per lane (rms_inv_warp's summation order: bit-identical)
+    const float inv = rms_inv_warp_cg(x + static_cast<size_t>(src_row) * d, d, eps, lane);
+#pragma unroll 4
     for (int i = lane; i < nv; i += 32) {
         const uint4 v = xr[i], g = wr[i];
         const uint32_t a[4] = {v.x, v.y, v.z, v.w};
@@ -235,7 +237,7 @@ cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows_idx, const __nv_
                     __nv_bfloat16* y, int n_rows, int d, float eps, cudaStream_t stream,
                     unsigned long long* zero_keys) {
     if (n_rows <= 0) return cudaSuccess;
-    const int warps = 8;
+    const int warps = 2;  // one warp per row, rows spread over many SMs (latency-bound)
     return launch_k(rmsnorm_kernel, dim3((n_rows + warps - 1) / warps), dim3(warps * 32), 0, stream, x,
                     rows_idx, w, y, n_rows, d, eps, zero_keys);
 }

@@ -300,6 +300,7 @@ struct asb_lane {
     // tensor maps of GEMM inputs: [0] box 128 (normal A), [1..4] box 32/64/128/256 (swap B)
     CUtensorMap map_h[7], map_attn[7], map_act[7], map_hl[7], map_q;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_switch = nullptr;  // orders a rebound stream after the old one (set_stream)
     bool launched = false;
     int last_logit_rows = 0;
     // per-category kernel timing (asb_lane_profile / asb_lane_stats)
@@ -356,6 +357,7 @@ struct asb_lane {
     ~asb_lane() {
         cudaSetDevice(m->device);
         if (launched) cudaStreamSynchronize(stream);
+        if (ev_switch) cudaEventDestroy(ev_switch);
         for (void* p : allocs) cudaFree(p);
         if (h_meta) cudaFreeHost(h_meta);
         if (h_out) cudaFreeHost(h_out);
@@ -824,7 +826,8 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->m = m;
         const ModelSpec& s = m->spec;
         L->max_T = max_tokens;
-        if (const char* e = std::getenv("ASB_DECODE_MAX_SPLITS")) L->max_splits = std::max(1, std::atoi(e));
+        // the fused last-arriver merge sums at most 16 split partials (decode_attn.cu): clamp
+        if (const char* e = std::getenv("ASB_DECODE_MAX_SPLITS")) L->max_splits = std::min(16, std::max(1, std::atoi(e)));
         L->max_segs = std::min(max_segments, max_tokens);
         L->max_tbl = L->max_segs * ((m->max_ctx + kBlockTokens - 1) / kBlockTokens);
         L->max_pitems = max_tokens / prefill_tokens_per_tile(s.hq, s.hkv) + L->max_segs;
@@ -908,13 +911,28 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
 
 void asb_lane_free(asb_lane* lane) { delete lane; }
 
+// Rebind without draining: the lane's in-flight forward (if any) keeps running on the old
+// partition; the new stream is ordered after it by an event (device-side wait, no host
+// block), so the lane's next launch still sees its previous one complete.  Cost: one event
+// record + one stream wait, a few microseconds ("< 50 us per rebinding").
 asb_status asb_lane_set_stream(asb_lane* lane, void* stream) {
     if (!lane || !stream) return ASB_ERR_INVALID_ARGUMENT;
-    if (lane->launched) cudaStreamSynchronize(lane->stream);
-    if (lane->own_stream) cudaStreamDestroy(lane->stream);
-    lane->own_stream = false;
-    lane->stream = static_cast<cudaStream_t>(stream);
-    return ASB_OK;
+    cudaStream_t ns = static_cast<cudaStream_t>(stream);
+    if (ns == lane->stream) return ASB_OK;
+    return guarded([&] {
+        if (lane->launched) {
+            if (!lane->ev_switch)
+                cuda_check(cudaEventCreateWithFlags(&lane->ev_switch, cudaEventDisableTiming), "event");
+            cuda_check(cudaEventRecord(lane->ev_switch, lane->stream), "rebind record");
+            cuda_check(cudaStreamWaitEvent(ns, lane->ev_switch, 0), "rebind wait");
+        }
+        if (lane->own_stream) {
+            // an owned stream is only replaced once; its pending work completes asynchronously
+            cuda_check(cudaStreamDestroy(lane->stream), "stream destroy");
+        }
+        lane->own_stream = false;
+        lane->stream = ns;
+    });
 }
 
 void* asb_lane_stream(const asb_lane* lane) { return lane ? lane->stream : nullptr; }
@@ -970,14 +988,37 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         std::vector<PrefillItem> pitems;
         int max_ctx = 0, max_pblocks = 0;
         int row = 0;
+        // Validate and size every segment before touching the registry: a failure (context
+        // limit, pool exhaustion, table overflow) leaves every length, block list and the
+        // free list exactly as they were.
+        {
+            std::map<uint32_t, int> grow;  // session -> tokens this call appends
+            int64_t tbl_need = 0, blocks_need = 0;
+            for (int i = 0; i < n_segs; ++i) {
+                const auto it = kv->sess.find(segs[i].session);
+                const int len0 = it == kv->sess.end() ? 0 : it->second.len;
+                const int start = len0 + grow[segs[i].session];
+                if (start + segs[i].n_tokens > m->max_ctx)
+                    fail(ASB_ERR_INFEASIBLE, "session " + std::to_string(segs[i].session) +
+                                                  " exceeds max_context");
+                grow[segs[i].session] += segs[i].n_tokens;
+                tbl_need += (start + segs[i].n_tokens + kBlockTokens - 1) / kBlockTokens;
+            }
+            if (tbl_need > L->max_tbl) fail(ASB_ERR_INVALID_ARGUMENT, "block tables exceed lane");
+            for (const auto& [sid, n] : grow) {
+                const auto it = kv->sess.find(sid);
+                const int len0 = it == kv->sess.end() ? 0 : it->second.len;
+                const int have = it == kv->sess.end() ? 0 : int(it->second.blocks.size());
+                blocks_need += std::max(0, (len0 + n + kBlockTokens - 1) / kBlockTokens - have);
+            }
+            if (blocks_need > int64_t(kv->free_list.size()))
+                fail(ASB_ERR_INFEASIBLE, "KV pool exhausted (" + std::to_string(kv->nb) + " blocks)");
+        }
         for (int i = 0; i < n_segs; ++i) {
             const asb_segment& g = segs[i];
             auto& ss = kv->get(g.session);
             const int start = ss.len;
-            if (start + g.n_tokens > m->max_ctx)
-                fail(ASB_ERR_INFEASIBLE, "session " + std::to_string(g.session) +
-                                              " exceeds max_context");
-            kv->ensure(ss, start + g.n_tokens);
+            kv->ensure(ss, start + g.n_tokens);  // cannot fail: sized above
             const int toff = int(tbl.size());
             tbl.insert(tbl.end(), ss.blocks.begin(), ss.blocks.end());
             for (int t = 0; t < g.n_tokens; ++t) {

@@ -1,87 +1,132 @@
 """The paper's policy ablation on real B200 kernels (the reference's CLI
 `compare` sweep, /root/reference/proj/tools/agentsim_main.cpp:171-259, run in wall-clock mode):
-every policy and the static Green Context split sweep serve the same synthetic agent trace
-through agsv_simulate, and we record TTFT/TPOT percentiles, throughput and the
-competitive-ratio verification summary.
+every policy (and the static Green Context split sweep) serves the same synthetic agent trace
+through agsv_simulate; we record TTFT/TPOT p50/p95/p99 pooled over reps, throughput, SLO
+attainment, rebind latency and the competitive-ratio verification summary.
 
-  python scripts/policy_compare.py [--config c2|c3] [--reps 2] [--out profiles/r1_policy_compare_c2.json]
+  python scripts/policy_compare.py --config c3 --reps 3 \
+      --runs agentserve mixed_fcfs agentserve:lend=0 agentserve:slack=2 static_partition:k=4 \
+      --out profiles/r2_policy_compare_c3.json
+
+A run spec is policy[:key=value,...] with keys lend (0/1), slack, tlow (theta_low / tau),
+calib (0/1: measured-curve calibration vs the reference's factor-8), k (static decode slots),
+unit (prefill launch-unit tokens), dt (control interval ms), r0 / rbase (initial / base
+decode slots).
 """
 import argparse
 import json
+import math
 import statistics
 import sys
+import tempfile
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-import bench  # noqa: E402
+from paper_2603_10342_b200 import workloads  # noqa: E402
 from paper_2603_10342_b200.agsv import Agsv  # noqa: E402
 
-ap = argparse.ArgumentParser()
-ap.add_argument("--config", choices=["c2", "c3", "c4"], default="c2")
-ap.add_argument("--reps", type=int, default=2)
-ap.add_argument("--out", default=None)
-ap.add_argument("--policies", nargs="*", default=None, help="subset, e.g. agentserve mixed_fcfs static_partition:3")
-ap.add_argument("--horizon-ms", type=float, default=None)
-a = ap.parse_args()
-api = Agsv()
 
-if a.config == "c2":
-    doc, src = bench.profile_doc(api)
-    base = bench.workload_config(1, 0, "wall", "agentserve", doc)
-elif a.config == "c4":  # C4: Qwen2.5-7B-shaped, 64 agents, 8k system prompts
-    prof = ROOT / "profiles" / "b200_profile_qwen2.5-7b.json"
-    d = json.loads(prof.read_text())
-    d.pop("measured", None)
-    base = {"workload": {"paradigm": "react", "model": "qwen2.5-7b", "concurrency": 64,
-                         "cold": {"min": 8192, "max": 8192, "mean": 8192},
-                         "resume": {"min": 256, "max": 256, "mean": 256}},
-            "slo": {"factor": 8.0, "tpot_stat": "p95"}, "policy": "agentserve", "seed": 13,
-            "profile": {"inline": d},
-            "backend": {"clock": "wall", "model": "qwen2.5-7b", "device": 0, "prefill_unit_tokens": 2048}}
-    src = str(prof.relative_to(ROOT))
-else:  # C3: Llama-3.2-3B-shaped, 32 ReAct agents
-    prof = ROOT / "profiles" / "b200_profile_llama3.2-3b.json"
-    d = json.loads(prof.read_text())
-    d.pop("measured", None)
-    base = {"workload": {"paradigm": "react", "model": "qwen2.5-3b", "concurrency": 32},
-            "slo": {"factor": 8.0, "tpot_stat": "p95"}, "policy": "agentserve", "seed": 13,
-            "profile": {"inline": d},
-            "backend": {"clock": "wall", "model": "llama3.2-3b", "device": 0, "prefill_unit_tokens": 2048}}
-    src = str(prof.relative_to(ROOT))
+def pct(xs, p):
+    if not xs:
+        return None
+    s = sorted(xs)
+    k = max(1, math.ceil(p / 100.0 * len(s)))
+    return s[min(k, len(s)) - 1]
 
-slots = json.loads(json.dumps(base["profile"]["inline"]))["total_sms"] // json.loads(json.dumps(base["profile"]["inline"]))["granularity"]
-runs = [("agentserve", None), ("mixed_fcfs", None), ("chunked_prefill", None), ("agentserve_no_slots", None)]
-runs += [("static_partition", k) for k in range(1, slots)]
-if a.policies:
-    want = [(x.split(":")[0], int(x.split(":")[1]) if ":" in x else None) for x in a.policies]
-    runs = [r for r in runs if r in want]
-rows = []
-for pol, k in runs:
-    cfg = json.loads(json.dumps(base))
-    cfg["policy"] = pol
-    if k is not None:
-        cfg["static_decode_slots"] = k
-    if a.horizon_ms:
-        cfg["horizon_ms"] = a.horizon_ms
-    ms = []
-    for _ in range(a.reps):
+
+def gaps_and_ttft(recs, metrics):
+    """Per-gap TPOT samples (the reference's collect_tokens, metrics.cpp:71-92) and TTFTs."""
+    gaps, prev = [], {}
+    for r in recs:
+        if r.get("k") == "issue" and r.get("req") == "decode":
+            prev[r["s"]] = None
+        elif r.get("k") == "step_done":
+            for s in r["emit"]:
+                if prev.get(s) is not None:
+                    gaps.append(r["t"] - prev[s])
+                prev[s] = r["t"]
+    ttft = [s["ttft_ms"] for s in metrics["sessions"] if s["ttft_ms"] >= 0]
+    return gaps, ttft
+
+
+def parse_spec(spec):
+    pol, _, rest = spec.partition(":")
+    kw = {}
+    for item in filter(None, rest.split(",")):
+        k, v = item.split("=")
+        kw[k] = float(v) if "." in v else int(v)
+    return pol, kw
+
+
+def run_spec(api, cfg_name, spec, reps, td, horizon=None):
+    pol, kw = parse_spec(spec)
+    cfg = workloads.run_config(cfg_name, policy=pol, lend=bool(kw.get("lend", 1)),
+                               calibrated=bool(kw.get("calib", 1)), slack=float(kw.get("slack", workloads.SLACK)),
+                               theta_low_frac=float(kw.get("tlow", 0.5)),
+                               static_slots=kw.get("k"), unit_tokens=int(kw.get("unit", 2048)))
+    if "dt" in kw:
+        cfg.setdefault("controller", {})["delta_t_ms"] = float(kw["dt"])
+    if "r0" in kw:
+        cfg.setdefault("controller", {})["initial_r_slots"] = int(kw["r0"])
+    if "rbase" in kw:
+        cfg.setdefault("controller", {})["r_base_slots"] = int(kw["rbase"])
+    if horizon:
+        cfg["horizon_ms"] = horizon
+    gaps, ttft, tps, att, reb, ends, tokens = [], [], [], [], [], [], 0
+    ver = None
+    for _ in range(reps):
         t = api.run(cfg)
-        ms.append((t.metrics(), t))
-    m0 = ms[-1][0]
-    ver = json.loads(ms[-1][1].verify()[0])
-    row = {"policy": pol, "static_decode_slots": k,
-           "throughput_tps": round(statistics.median(m["throughput_tps"] for m, _ in ms), 1),
-           "ttft_p50_ms": round(statistics.median(m["ttft_p50_ms"] for m, _ in ms), 3),
-           "ttft_p99_ms": round(statistics.median(m["ttft_p99_ms"] for m, _ in ms), 3),
-           "tpot_p50_ms": round(statistics.median(m["tpot_p50_ms"] for m, _ in ms), 3),
-           "tpot_p99_ms": round(statistics.median(m["tpot_p99_ms"] for m, _ in ms), 3),
-           "slo_attainment": m0.get("slo_attainment", m0.get("joint_slo_attainment")),
+        m = t.metrics()
+        recs = [json.loads(x) for x in t.jsonl(td).splitlines()]
+        g, tt = gaps_and_ttft(recs, m)
+        gaps += g
+        ttft += tt
+        tps.append(m["throughput_tps"])
+        att.append(m.get("slo_attainment", m.get("joint_slo_attainment")))
+        dev = recs[-1].get("device", {})
+        reb.append(dev.get("rebind_us", {}))
+        ends.append(recs[-1]["end_ms"])
+        tokens += sum(len(r["emit"]) for r in recs if r.get("k") == "step_done")
+        ver = json.loads(t.verify()[0])
+    row = {"run": spec, "policy": pol, **{k: v for k, v in kw.items()},
+           "tokens_per_s": round(1000.0 * tokens / sum(ends), 1),
+           "ttft_ms": {p: round(pct(ttft, p), 3) for p in (50, 95, 99)},
+           "tpot_ms": {p: round(pct(gaps, p), 3) for p in (50, 95, 99)},
+           "slo_attainment": statistics.mean(a for a in att if a is not None) if any(a is not None for a in att) else None,
+           "rebind_us": reb[-1],
+           "slo": cfg.get("slo"), "controller": cfg.get("controller"),
            "verify": {"checked": ver["checked"], "vacuous": ver["vacuous"], "violations": ver["violations"],
-                      "min_rho": ver["min_rho"], "assumptions_met": ver["assumptions_met"]}}
-    rows.append(row)
-    print(json.dumps(row), flush=True)
-doc = {"config": a.config, "profile": src, "reps": a.reps, "clock": "wall (B200, Green Context partitions)",
-       "runs": rows}
-if a.out:
-    Path(a.out).write_text(json.dumps(doc, indent=1))
+                      "min_rho": ver["min_rho"], "assumptions_met": ver["assumptions_met"]},
+           "samples": {"sessions": len(ttft), "tpot_gaps": len(gaps)}}
+    return row
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", choices=sorted(workloads.CONFIGS), default="c3")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--runs", nargs="*", default=None)
+    ap.add_argument("--static-sweep", action="store_true")
+    ap.add_argument("--horizon-ms", type=float, default=None)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    api = Agsv()
+    td = tempfile.mkdtemp()
+    runs = a.runs or ["agentserve", "mixed_fcfs", "chunked_prefill", "agentserve_no_slots"]
+    if a.static_sweep:
+        prof, _ = workloads.load_profile(workloads.CONFIGS[a.config]["model"])
+        runs += [f"static_partition:k={k}" for k in range(1, prof["total_sms"] // prof["granularity"])]
+    rows = []
+    for spec in runs:
+        row = run_spec(api, a.config, spec, a.reps, td, a.horizon_ms)
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    doc = {"config": a.config, "label": workloads.CONFIGS[a.config]["label"], "reps": a.reps,
+           "clock": "wall (B200, Green Context partitions)", "runs": rows}
+    if a.out:
+        Path(a.out).write_text(json.dumps(doc, indent=1) + "\n")
+
+
+if __name__ == "__main__":
+    main()

@@ -80,3 +80,26 @@ def test_pool_exhaustion_is_infeasible_not_a_crash(model):
     lane = Lane(model, max_tokens=512, max_segments=8)
     st = _status(lambda: lane.forward(kv, [(0, 200, 0)], np.zeros(200, dtype=np.int32)))
     assert st == 6  # ASB_ERR_INFEASIBLE
+
+
+def test_failed_forward_leaves_registry_untouched(model):
+    """A forward that fails part-way (pool exhaustion on its second segment, max_context on a
+    the lane limit) must not half-commit: lengths, block tables and the free list are unchanged,
+    and the next forward writes at the right positions (runtime.cu asb_forward)."""
+    kv = KvPool(model, num_blocks=4)
+    lane = Lane(model, max_tokens=1024, max_segments=8)
+    lane.forward(kv, [(0, 64, 0)], np.zeros(64, dtype=np.int32))
+    lane.wait()
+    before = (kv.length(0), kv.block_table(0), kv.free_blocks())
+    # session 0 grows by one block (fits), session 1 needs 4 blocks (does not): whole call fails
+    st = _status(lambda: lane.forward(kv, [(0, 10, 0), (1, 200, 0)], np.zeros(210, dtype=np.int32)))
+    assert st == 6
+    assert (kv.length(0), kv.block_table(0), kv.free_blocks()) == before
+    assert kv.length(1) == 0 and kv.block_table(1) == []
+    # over the lane's token limit: rejected before any registry change
+    st = _status(lambda: lane.forward(kv, [(0, 1, 0), (2, 5000, 0)], np.zeros(5001, dtype=np.int32)))
+    assert st != 0
+    assert (kv.length(0), kv.block_table(0), kv.free_blocks()) == before
+    lane.forward(kv, [(0, 1, 1)], np.zeros(1, dtype=np.int32))
+    lane.wait()
+    assert kv.length(0) == 65
