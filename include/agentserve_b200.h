@@ -130,7 +130,7 @@ enum {
     ASB_STAT_DECODE_GEMM = 2,  /* units: weight + activation bytes (swap-AB path) */
     ASB_STAT_PREFILL_GEMM = 3, /* units: FLOPs */
     ASB_STAT_FORWARD = 4,      /* whole forward; units: tokens */
-    ASB_STAT_DECODE_STEP = 5,  /* persistent decode-step kernel; units: weight + K/V bytes */
+    ASB_STAT_DECODE_STEP = 5,  /* reserved (the persistent decode-step kernel was removed) */
     ASB_STAT_COUNT = 6
 };
 asb_status asb_lane_profile(asb_lane* lane, int enable);
@@ -170,9 +170,6 @@ asb_status asb_slots_sm_counts(const asb_slots* s, int decode_level, int* decode
 /* ASB_GEMM_TIMELINE=1: per-CTA globaltimer stamps (start, MMA done, epilogue done, exit) of the
  * lane's most recent GEMM launch, [148][4] ns. */
 asb_status asb_debug_gemm_timeline(asb_lane* lane, unsigned long long* out, int n);
-/* ASB_MK_TIMELINE=1 at lane creation: globaltimer (ns) at the start of every phase of the
- * lane's most recent persistent decode-step launch, [num_sms][256] (slot 255 = CTA exit). */
-asb_status asb_debug_mk_timeline(asb_lane* lane, unsigned long long* out, int n);
 /* ASB_ATTN_TIMELINE=1 at lane creation: per-CTA globaltimer stamps [1024][8] of the last decode
  * attention launch of the lane's most recent forward (entry, after pdl wait, first K/V
  * sub-block, consumers done, partial written, exit). */

@@ -87,7 +87,6 @@ SIGNATURES = {
     "asb_lane_profile": (I, [P, I]),
     "asb_lane_stats": (I, [P, I, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64), I]),
     "asb_lane_set_sms": (I, [P, I]),
-    "asb_debug_mk_timeline": (I, [P, C.POINTER(C.c_ulonglong), I]),
     "asb_debug_attn_timeline": (I, [P, C.POINTER(C.c_ulonglong), I]),
     "asb_lane_counters": (I, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64), I]),
 }

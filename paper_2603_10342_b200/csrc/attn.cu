@@ -174,10 +174,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
             const uint64_t pol = policy_evict_last();  // pages are re-read by the other heads
             for (int j = 0; j < n_kv; ++j) {
                 const int st = j % C::kStages;
+                const int blk = table[blk0 + j];  // issued before the wait: off the refill path
                 mbar_wait(&kv_empty[st], ((j / C::kStages) & 1) ^ 1);
                 mbar_expect_tx(&kv_full[st], C::kStageBytes);
-                const int blk = table[blk0 + j];
-                const int row = ((s.layer * s.num_blocks + blk) * s.hkv + kvh) * kBlockTokens;
+                const int row = ((s.layer * s.num_blocks + blk) * s.hkv + kvh) * kKvPageRows;
                 uint8_t* kdst = skv + st * C::kStageBytes;
                 uint8_t* vdst = kdst + C::kKBytes;
 #pragma unroll

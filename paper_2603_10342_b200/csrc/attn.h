@@ -8,10 +8,10 @@
 
 namespace asb {
 
-// Paged KV cache geometry. One bf16 pool for K and one for V, laid out
-//   [layer][block][kv_head][kBlockTokens][head_dim]
-// so one KV block of one head is a contiguous 64 x head_dim tile (8 or 16 KiB):
-// a single TMA box for prefill attention and a 128-bit-coalesced stream for decode.
+// Paged KV cache geometry.  One bf16 pool, laid out
+//   [layer][block][kv_head][K: kBlockTokens rows | V: kBlockTokens rows][head_dim]
+// so one KV block of one head is a contiguous 64 x head_dim K tile followed by its V tile
+// (8 or 16 KiB each): a single TMA box each for prefill attention, one box for both in decode.
 constexpr int kBlockTokens = 64;
 
 // One prefill-attention work item: up to prefill_tokens_per_cta() query tokens of one
@@ -32,12 +32,18 @@ struct DecodeItem {
     int pad;
 };
 
+// KV pool page layout: [layer][block][kv_head][K rows 0..63 | V rows 0..63][hd] bf16 -- the K and
+// V pages of one (block, head) are adjacent, so a decode sub-block (32 tokens of K and of V)
+// is one 16 KiB (hd 128) TMA request; kKvPageRows rows separate consecutive (block, head) pages.
+constexpr int kKvPageRows = 2 * kBlockTokens;
+
 struct AttnShape {
     int hq, hkv, hd;
     int num_blocks;   // blocks per layer in the pool
     int layer;        // layer index (selects the pool slice)
     float scale_log2; // log2(e) / sqrt(hd)
     unsigned long long* dbg = nullptr;  // decode attention: per-CTA globaltimer stamps [cta][8]
+    int dbg_load_only = 0;  // decode attention timing ablation: consumers skip the math
 };
 
 // grid = (items, hkv, splits).  Split-KV over gridDim.z when the grid is small (resume
@@ -72,6 +78,6 @@ cudaError_t decode_attention(const CUtensorMap& tmap_k32, const CUtensorMap& tma
                              float* part_o, float* part_ml, int* counters, int max_splits, int num_sms,
                              const AttnShape& s, cudaStream_t stream);
 
-int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits);
+int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits, int ctas_per_sm, int warps);
 
 }  // namespace asb

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                 mbar_expect_tx(&full[st], C::kStage);
                 const int j = s0 + i;
                 const int blk = table[j >> 1];
-                const int row = ((s.layer * s.num_blocks + blk) * s.hkv + kvh) * kBlockTokens + (j & 1) * kSub;
+                const int row = ((s.layer * s.num_blocks + blk) * s.hkv + kvh) * kKvPageRows + (j & 1) * kSub;
                 uint8_t* kd = ring + st * C::kStage;
                 uint8_t* vd = kd + C::kTile;
 #pragma unroll
@@ -170,6 +170,11 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         const int st = stage_of(i, kWarpsR, kStagesR);
         mbar_wait(&full[st], (i / kStagesR) & 1);
         if (i == 0 && lane == 0) stamp(2);
+        if (s.dbg_load_only) {  // timing ablation (ASB_DEBUG_SKIP=attnmath): the load stream alone
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            continue;
+        }
         const uint32_t kt = smem_u32(ring + st * C::kStage);
         const uint32_t vt = kt + C::kTile;
         // ---- S = Q K^T : 4 n-tiles of 8 keys

@@ -14,10 +14,11 @@ __device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __e
 
 __device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
-// element offset of (slot, kv_head) in a paged K or V pool (layout of attn.h)
+// element offset of (slot, kv_head) from the K (k_pool) or V (v_pool = k_pool + one page)
+// base of the interleaved paged pool (layout of attn.h)
 __device__ __forceinline__ size_t pool_off(const RopeEpi& R, int slot, int kv_head) {
     const int blk = slot / kBlockTokens, off = slot % kBlockTokens;
-    return ((((size_t)R.layer * R.num_blocks + blk) * R.hkv + kv_head) * kBlockTokens + off) * R.hd;
+    return ((((size_t)R.layer * R.num_blocks + blk) * R.hkv + kv_head) * kKvPageRows + off) * R.hd;
 }
 
 // rotate_half pair at one cos/sin column

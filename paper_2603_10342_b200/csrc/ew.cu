@@ -168,7 +168,7 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv,
         } else {
             const int kh = h - hq;
             __nv_bfloat16* kd =
-                k_pool + (((static_cast<size_t>(layer) * num_blocks + blk) * hkv + kh) * kBlockTokens + off) * hd;
+                k_pool + (((static_cast<size_t>(layer) * num_blocks + blk) * hkv + kh) * kKvPageRows + off) * hd;
             kd[j] = __float2bfloat16_rn(y1);
             kd[j + half] = __float2bfloat16_rn(y2);
         }
@@ -176,7 +176,7 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv,
     for (int i = threadIdx.x; i < hkv * hd; i += blockDim.x) {
         const int h = i / hd, j = i % hd;
         __nv_bfloat16* vd =
-            v_pool + (((static_cast<size_t>(layer) * num_blocks + blk) * hkv + h) * kBlockTokens + off) * hd;
+            v_pool + (((static_cast<size_t>(layer) * num_blocks + blk) * hkv + h) * kKvPageRows + off) * hd;
         vd[j] = row[(hq + hkv + h) * hd + j];
     }
 }

@@ -114,6 +114,9 @@ bool make_tmap_packed(CUtensorMap* out, const void* base, int rows_padded, int c
 // 3-D view (64 cols, rows, k-block) of a row-major bf16 [rows][cols] activation, box
 // [2 k-blocks][box_rows][64], SWIZZLE_128B: both k-blocks of a decode GEMM stage in one request.
 bool make_tmap_act_kpair(CUtensorMap* out, const void* base, int rows, int cols, int box_rows);
+// 5-D map over the interleaved KV pool (attn.h): box [K,V][hd/64][box_rows][64] SWIZZLE_128B,
+// i.e. box_rows tokens of one page's K and V in one request (coords: 0, row, 0, 0, page).
+bool make_tmap_kv_sub(CUtensorMap* out, const void* base, long pages, int hd, int page_rows, int box_rows);
 // 3-D bf16 map over [d2][d1][d0] (d0 contiguous), box = [b2][b1][64], SWIZZLE_128B.
 bool make_tmap_bf16_3d(CUtensorMap* out, const void* base, int d0, int d1, int d2, int b1, int b2);
 // 2-D bf16 tensor map, row-major [rows][cols], box = [box_rows][64 cols], SWIZZLE_128B.

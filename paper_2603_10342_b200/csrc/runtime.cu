@@ -23,7 +23,6 @@
 
 #include "../../include/agentserve_b200.h"
 #include "attn.h"
-#include "decode_step.h"
 #include "ew.h"
 #include "gemm.h"
 #include "launch.cuh"
@@ -200,7 +199,6 @@ struct asb_model {
     };
     std::vector<Layer> layers;
     float *cos_t = nullptr, *sin_t = nullptr;
-    MkLayer* mk_layers = nullptr;  // device copy of the per-layer pointers (decode-step kernel)
 
     ~asb_model() {
         cudaSetDevice(device);
@@ -235,7 +233,8 @@ constexpr float kAmpN = 0.1f;
 struct asb_kv {
     asb_model* m = nullptr;
     int nb = 0;
-    __nv_bfloat16 *k_pool = nullptr, *v_pool = nullptr;
+    __nv_bfloat16* pool = nullptr;  // interleaved K|V pages (attn.h)
+    __nv_bfloat16 *k_pool = nullptr, *v_pool = nullptr;  // pool, pool + one page (element views)
     CUtensorMap tk, tv;      // box 64 rows (prefill attention)
     CUtensorMap tk32, tv32;  // box 32 rows (decode attention sub-blocks)
     std::vector<int> free_list;  // LIFO: back() is handed out next
@@ -249,8 +248,7 @@ struct asb_kv {
 
     ~asb_kv() {
         cudaSetDevice(m->device);
-        cudaFree(k_pool);
-        cudaFree(v_pool);
+        cudaFree(pool);
     }
     Sess& get(uint32_t s) { return sess[s]; }
     void ensure(Sess& s, int new_len) {
@@ -277,16 +275,7 @@ struct asb_lane {
     // split merge inside the decode-attention kernel (last-arriving split) instead of a
     // combine launch; ASB_ATTN_COMBINE=1 selects the separate combine kernel
     bool attn_fused_merge = std::getenv("ASB_ATTN_COMBINE") == nullptr;
-    // persistent decode-step kernel (decode_step.cu): grid barrier, split-tile and attention
-    // workspaces; mega = 0 after a failed cooperative launch (kernel-per-op path from then on)
-    unsigned* mk_bar = nullptr;
-    int* mk_tile_cnt = nullptr;
-    float *mk_ws = nullptr, *mk_apo = nullptr, *mk_apml = nullptr;
-    int* mk_acnt = nullptr;
-    int mk_max_spl = 16;
-    unsigned long long* mk_dbg = nullptr;  // ASB_MK_TIMELINE=1: per-CTA phase start stamps
     unsigned long long* attn_dbg = nullptr;  // ASB_ATTN_TIMELINE=1: decode-attention CTA stamps
-    bool mega = std::getenv("ASB_MEGA") != nullptr && std::atoi(std::getenv("ASB_MEGA")) != 0;  // opt-in
     CUtensorMap map_x[7];
     bool pdl = std::getenv("ASB_NO_PDL") == nullptr;  // programmatic dependent launch
     unsigned long long* dbg_times = nullptr;  // ASB_GEMM_TIMELINE: per-CTA stamps of the last GEMM
@@ -639,15 +628,6 @@ asb_status asb_model_create(const char* model, uint64_t seed, int device, int ma
         m->sin_t = static_cast<float*>(dmalloc(sn.size() * 4, m->allocs));
         cuda_check(cudaMemcpy(m->cos_t, c.data(), c.size() * 4, cudaMemcpyHostToDevice), "copy rope");
         cuda_check(cudaMemcpy(m->sin_t, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice), "copy rope");
-        {
-            std::vector<MkLayer> mk;
-            for (const auto& ly : m->layers)
-                mk.push_back(MkLayer{ly.qkv.ptr, ly.o.ptr, ly.gate_up.ptr, ly.down.ptr, ly.attn_norm, ly.mlp_norm,
-                                     ly.qkv_bias});
-            m->mk_layers = static_cast<MkLayer*>(dmalloc(mk.size() * sizeof(MkLayer), m->allocs));
-            cuda_check(cudaMemcpy(m->mk_layers, mk.data(), mk.size() * sizeof(MkLayer), cudaMemcpyHostToDevice),
-                       "copy layer table");
-        }
         cuda_check(cudaDeviceSynchronize(), "weight init");
         *out = m.release();
     });
@@ -690,18 +670,22 @@ asb_status asb_kv_create(asb_model* m, int num_blocks, asb_kv** out) {
         kv->m = m;
         kv->nb = num_blocks;
         const ModelSpec& s = m->spec;
-        const size_t elems = size_t(s.layers) * num_blocks * s.hkv * kBlockTokens * s.hd;
-        cuda_check(cudaMalloc(&kv->k_pool, elems * 2), "cudaMalloc K pool");
-        cuda_check(cudaMalloc(&kv->v_pool, elems * 2), "cudaMalloc V pool");
-        // zero so masked tail rows of a block are finite (0 * garbage must not be NaN)
-        cuda_check(cudaMemset(kv->k_pool, 0, elems * 2), "memset");
-        cuda_check(cudaMemset(kv->v_pool, 0, elems * 2), "memset");
-        const long rows = long(s.layers) * num_blocks * s.hkv * kBlockTokens;
+        const size_t pages = size_t(s.layers) * num_blocks * s.hkv;
+        const size_t elems = pages * kKvPageRows * s.hd;
+        cuda_check(cudaMalloc(&kv->pool, elems * 2), "cudaMalloc KV pool");
+        // zeroed so that masked tail rows of a partial block are finite
+        cuda_check(cudaMemset(kv->pool, 0, elems * 2), "memset");
+        kv->k_pool = kv->pool;
+        kv->v_pool = kv->pool + size_t(kBlockTokens) * s.hd;
+        const long rows = long(pages) * kKvPageRows;
         if (rows >= (1l << 31)) fail(ASB_ERR_VALIDATION, "KV pool too large for 32-bit TMA rows");
+        // [64 rows][64 cols] (prefill attention) and [32 rows][64 cols] (decode sub-blocks)
+        // boxes of the K pages (row = page*128 + t on the k_pool view) and the V pages (the
+        // same row index on the v_pool view, one page further)
         if (!make_tmap_bf16(&kv->tk, kv->k_pool, int(rows), s.hd, s.hd, kBlockTokens) ||
-            !make_tmap_bf16(&kv->tv, kv->v_pool, int(rows), s.hd, s.hd, kBlockTokens) ||
+            !make_tmap_bf16(&kv->tv, kv->v_pool, int(rows - kBlockTokens), s.hd, s.hd, kBlockTokens) ||
             !make_tmap_bf16(&kv->tk32, kv->k_pool, int(rows), s.hd, s.hd, 32) ||
-            !make_tmap_bf16(&kv->tv32, kv->v_pool, int(rows), s.hd, s.hd, 32))
+            !make_tmap_bf16(&kv->tv32, kv->v_pool, int(rows - kBlockTokens), s.hd, s.hd, 32))
             fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for the KV pool");
         kv->free_list.reserve(num_blocks);
         for (int b = num_blocks - 1; b >= 0; --b) kv->free_list.push_back(b);
@@ -806,7 +790,7 @@ asb_status asb_kv_read_token(const asb_kv* kv, uint32_t session, int position, u
         for (int l = 0; l < s.layers; ++l)
             for (int h = 0; h < s.hkv; ++h) {
                 const size_t src =
-                    (((size_t(l) * kv->nb + blk) * s.hkv + h) * kBlockTokens + off) * s.hd;
+                    (((size_t(l) * kv->nb + blk) * s.hkv + h) * kKvPageRows + off) * s.hd;
                 const size_t dst = (size_t(l) * s.hkv + h) * s.hd;
                 cuda_check(cudaMemcpy(k_out + dst, kv->k_pool + src, s.hd * 2, cudaMemcpyDeviceToHost), "copy");
                 cuda_check(cudaMemcpy(v_out + dst, kv->v_pool + src, s.hd * 2, cudaMemcpyDeviceToHost), "copy");
@@ -860,25 +844,9 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         cuda_check(cudaMemset(L->post_cnt, 0, 64), "counters");
         cuda_check(cudaMemset(L->dcnt, 0, size_t(dec_rows) * s.hkv * 4), "counters");
         {
-            const int rows = kMkMaxRows, G = s.hq / s.hkv;
-            const int max_n = std::max({s.vocab, 2 * s.ffn, (s.hq + 2 * s.hkv) * s.hd, s.d});
-            L->mk_bar = static_cast<unsigned*>(dmalloc(256, L->allocs));  // [0] arrivals, [32] generation
-            L->mk_tile_cnt = static_cast<int*>(dmalloc(size_t(max_n / 128 + 2) * 4, L->allocs));
-            L->mk_ws = static_cast<float*>(dmalloc(size_t(m->num_sms) * 2 * 128 * 32 * 4, L->allocs));
-            L->mk_apo = static_cast<float*>(dmalloc(size_t(rows) * s.hkv * L->mk_max_spl * G * s.hd * 4, L->allocs));
-            L->mk_apml = static_cast<float*>(dmalloc(size_t(rows) * s.hkv * L->mk_max_spl * G * 2 * 4, L->allocs));
-            L->mk_acnt = static_cast<int*>(dmalloc(size_t(rows) * s.hkv * 4, L->allocs));
-            cuda_check(cudaMemset(L->mk_bar, 0, 256), "mk");
-            cuda_check(cudaMemset(L->mk_tile_cnt, 0, size_t(max_n / 128 + 2) * 4), "mk");
-            cuda_check(cudaMemset(L->mk_acnt, 0, size_t(rows) * s.hkv * 4), "mk");
             if (std::getenv("ASB_ATTN_TIMELINE")) {
                 L->attn_dbg = static_cast<unsigned long long*>(dmalloc(1024 * 8 * 8, L->allocs));
                 cuda_check(cudaMemset(L->attn_dbg, 0, 1024 * 8 * 8), "attn dbg");
-            }
-            if (std::getenv("ASB_MK_TIMELINE")) {
-                L->mk_dbg = static_cast<unsigned long long*>(
-                    dmalloc(size_t(m->num_sms) * kMkDbgSlots * 8, L->allocs));
-                cuda_check(cudaMemset(L->mk_dbg, 0, size_t(m->num_sms) * kMkDbgSlots * 8), "mk");
             }
         }
         // split-KV partials for small prefill grids (resume chunks): <= 4096 rows of 128 queries
@@ -1081,6 +1049,11 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         as.hd = s.hd;
         as.num_blocks = kv->nb;
         as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(s.hd)));
+        {
+            static const bool load_only = std::getenv("ASB_DEBUG_SKIP") &&
+                                          std::string(std::getenv("ASB_DEBUG_SKIP")).find("attnmath") != std::string::npos;
+            as.dbg_load_only = load_only ? 1 : 0;
+        }
         if (L->attn_dbg) {
             cuda_check(cudaMemsetAsync(L->attn_dbg, 0, 1024 * 8 * 8, L->stream), "attn dbg");
             as.dbg = L->attn_dbg;
@@ -1101,76 +1074,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         cudaEvent_t fwd_a = L->prof ? L->take_event() : nullptr;
         if (fwd_a) cuda_check(cudaEventRecord(fwd_a, st), "event");
         PdlScope pdl_scope(L->pdl && !L->prof);
-        // Decode-only steps of <= 16 rows: one persistent launch for the whole forward
-        // (decode_step.cu).  A failed cooperative launch (partition too small for the grid)
-        // switches the lane to the kernel-per-op path below for good.
-        bool mega_done = false;
-        if (L->mega && pitems.empty() && int(ditems.size()) == n_segs && T <= kMkMaxRows && n_logit == T &&
-            s.hq / s.hkv <= 8 && (s.hd == 64 || s.hd == 128) && s.d % 64 == 0 && s.d <= 1024 && s.ffn % 64 == 0 &&
-            (s.hq * s.hd) % 64 == 0 && std::getenv("ASB_DEBUG_SKIP") == nullptr) {
-            MkMaps mm{L->map_x[1], L->map_attn[1], L->map_act[1], kv->tk32, kv->tv32};
-            MkParams mp{};
-            mp.layers = m->mk_layers;
-            mp.L = s.layers;
-            mp.d = s.d;
-            mp.hq = s.hq;
-            mp.hkv = s.hkv;
-            mp.hd = s.hd;
-            mp.ffn = s.ffn;
-            mp.vocab = s.vocab;
-            mp.eps = s.eps;
-            mp.scale_log2 = as.scale_log2;
-            mp.T = T;
-            mp.G = std::min(L->n_sms(), m->num_sms);
-            const int n_items = T * s.hkv;
-            mp.attn_spl = std::max(1, std::min({mp.G / n_items, L->mk_max_spl, (max_ctx + 31) / 32}));
-            mp.tok = d_tok;
-            mp.pos = d_pos;
-            mp.slot = d_slot;
-            mp.items = d_ditems;
-            mp.tables = d_tbl;
-            mp.embed = m->embed.ptr;
-            mp.lm_head = m->lm_head.ptr;
-            mp.final_norm = m->final_norm;
-            mp.x = L->x;
-            mp.q = L->q;
-            mp.attn = L->attn;
-            mp.act = L->act;
-            mp.logits = L->logits;
-            mp.keys = L->d_out;
-            mp.k_pool = kv->k_pool;
-            mp.v_pool = kv->v_pool;
-            mp.num_blocks = kv->nb;
-            mp.cos_t = m->cos_t;
-            mp.sin_t = m->sin_t;
-            mp.bar = L->mk_bar;
-            mp.tile_cnt = L->mk_tile_cnt;
-            mp.ws = L->mk_ws;
-            mp.apart_o = L->mk_apo;
-            mp.apart_ml = L->mk_apml;
-            mp.acnt = L->mk_acnt;
-            mp.dbg = L->mk_dbg;
-            // algorithmic bytes: every weight once + every context token's K and V once
-            double wbytes = 2.0 * double(m->lm_head.rows) * m->lm_head.cols;
-            for (const auto& ly : m->layers)
-                wbytes += 2.0 * (double(ly.qkv.rows) * ly.qkv.cols + double(ly.o.rows) * ly.o.cols +
-                                 double(ly.gate_up.rows) * ly.gate_up.cols + double(ly.down.rows) * ly.down.cols);
-            cudaError_t e = cudaSuccess;
-            L->timed(ASB_STAT_DECODE_STEP, wbytes + dattn_bytes * s.layers,
-                     [&] { e = decode_step_launch(mm, mp, st); });
-            if (e == cudaSuccess) {
-                mega_done = true;
-                L->n_launch += 1;
-                cuda_check(cudaMemcpyAsync(L->h_out, L->d_out, n_logit * 8, cudaMemcpyDeviceToHost, st), "ids D2H");
-                L->d2h += int64_t(n_logit) * 8;
-            } else {
-                cudaGetLastError();
-                L->mega = false;
-                std::fprintf(stderr, "[agentserve_b200] decode-step kernel unavailable (%s, grid %d): "
-                             "kernel-per-op decode from now on\n", cudaGetErrorString(e), mp.G);
-            }
-        }
-        if (!mega_done) {
+        {
             // the fused QKV epilogue needs q/k/v regions aligned to the 128-row weight tiles
             // ASB_DEBUG_SKIP=attn,norm,...: timing ablation only (outputs are garbage)
             static const std::string skip_list = std::getenv("ASB_DEBUG_SKIP") ? std::getenv("ASB_DEBUG_SKIP") : "";
@@ -1320,17 +1224,6 @@ asb_status asb_debug_gemm_timeline(asb_lane* L, unsigned long long* out, int n) 
     return guarded([&] {
         cuda_check(cudaStreamSynchronize(L->stream), "timeline");
         cuda_check(cudaMemcpy(out, L->dbg_times, size_t(std::min(n, 148 * 8)) * 8, cudaMemcpyDeviceToHost), "timeline");
-    });
-}
-
-asb_status asb_debug_mk_timeline(asb_lane* L, unsigned long long* out, int n) {
-    if (!L || !out) return ASB_ERR_INVALID_ARGUMENT;
-    return guarded([&] {
-        if (!L->mk_dbg) fail(ASB_ERR_NO_DATA, "lane created without ASB_MK_TIMELINE=1");
-        cuda_check(cudaStreamSynchronize(L->stream), "sync");
-        const size_t total = size_t(L->m->num_sms) * kMkDbgSlots;
-        cuda_check(cudaMemcpy(out, L->mk_dbg, std::min<size_t>(total, size_t(n)) * 8, cudaMemcpyDeviceToHost),
-                   "timeline");
     });
 }
 

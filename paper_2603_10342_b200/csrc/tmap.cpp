@@ -75,6 +75,23 @@ bool make_tmap_packed(CUtensorMap* out, const void* base, int rows_padded, int c
     return r == CUDA_SUCCESS;
 }
 
+bool make_tmap_kv_sub(CUtensorMap* out, const void* base, long pages, int hd, int page_rows, int box_rows) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    const int halves = hd / 64;
+    // (col within a 64-col half, row within a K or V page, half, K|V, page)
+    cuuint64_t dims[5] = {64, static_cast<cuuint64_t>(page_rows), static_cast<cuuint64_t>(halves), 2,
+                          static_cast<cuuint64_t>(pages)};
+    const cuuint64_t row_b = static_cast<cuuint64_t>(hd) * 2;
+    cuuint64_t strides[4] = {row_b, 128, row_b * page_rows, row_b * page_rows * 2};
+    cuuint32_t box[5] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(halves), 2, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 bool make_tmap_act_kpair(CUtensorMap* out, const void* base, int rows, int cols, int box_rows) {
     EncodeFn enc = get_encode();
     if (!enc) return false;

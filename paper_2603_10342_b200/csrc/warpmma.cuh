@@ -1,5 +1,5 @@
 // Legacy warp-level tensor-core helpers (mma.sync m16n8k16, ldmatrix) and the SW128 tile
-// addressing shared by the memory-bound decode kernels (decode_attn.cu, decode_step.cu), where
+// addressing shared by the memory-bound decode kernels (decode_attn.cu, dgemv.cu), where
 // a register-resident warp MMA beats a TMEM round trip for M <= 16-row problems.
 #pragma once
 #include <cstdint>
@@ -24,10 +24,13 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(addr));
 }
-// D = A (16x16 bf16, row) * B (16x8 bf16, col) + D, fp32 accumulate
+// D = A (16x16 bf16, row) * B (16x8 bf16, col) + D, fp32 accumulate.  Not volatile: a pure
+// register function, so the compiler may interleave independent MMAs with the ldmatrix loads
+// of the next k-step (volatile pinned every MMA behind the load just before it, serialising
+// load latency and MMA latency).  Accumulation order is fixed by the data dependence.
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
         "{%8,%9}, {%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])

@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--decode", nargs="*", default=None, help="override decode cases, e.g. 16x3000 48x3000")
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--level", type=int, default=0,
+                    help="run the decode cases on the decode partition of this Green Context slot level")
     a = ap.parse_args()
     results = []
     rng = np.random.default_rng(0)
@@ -72,6 +74,14 @@ def main():
                             "forward_ms": st["forward"][0] / a.reps})
             print(json.dumps(results[-1]), flush=True)
         # decode
+        dlane, sms = lane, 148
+        if a.level:
+            from paper_2603_10342_b200.device import Slots
+            slots = Slots(0, levels=9, granularity=16)
+            sd, _ = slots.bind(a.level)
+            sms = slots.sm_counts(a.level)[0]
+            dlane = Lane(m, max_tokens=pmax, max_segments=80, stream=sd)
+            dlane.set_sms(sms)
         for B, ctx in dcs:
             sess = list(range(B))
             for s in sess:
@@ -81,15 +91,24 @@ def main():
                     lane.forward(kv, [(s, n, 0)], rng.integers(0, V, n))
                     done += n
             lane.wait()
-            lane.stats()
-            lane.profile(True)
+            for rep in range(2):  # warm
+                dlane.forward(kv, [(s, 1, 1) for s in sess], rng.integers(0, V, B))
+                dlane.wait()
+            dlane.stats()
+            dlane.profile(True)
             for rep in range(a.reps):
-                lane.forward(kv, [(s, 1, 1) for s in sess], rng.integers(0, V, B))
-                lane.wait()
-            st = lane.stats()
-            lane.profile(False)
+                dlane.forward(kv, [(s, 1, 1) for s in sess], rng.integers(0, V, B))
+                dlane.wait()
+            st = dlane.stats()
+            dlane.profile(False)
+            step_ms = []
+            for rep in range(a.reps):  # unprofiled (PDL on)
+                dlane.forward(kv, [(s, 1, 1) for s in sess], rng.integers(0, V, B))
+                dlane.wait()
+                step_ms.append(dlane.last_ms())
             da, dg = st["decode_attn"], st["decode_gemm"]
-            results.append({"model": name, "case": f"decode B={B} ctx={ctx}",
+            results.append({"model": name, "case": f"decode B={B} ctx={ctx}", "sms": sms,
+                            "step_ms_unprofiled": float(np.median(step_ms)),
                             "decode_attn_gbs": rate(da[0], da[1], "bytes"),
                             "decode_attn_frac": rate(da[0], da[1], "bytes") / PEAKS["hbm_gbs"],
                             "decode_attn_us_per_layer": 1000 * da[0] / max(1, da[2]),
@@ -99,7 +118,7 @@ def main():
             print(json.dumps(results[-1]), flush=True)
             for s in sess:
                 kv.release(s)
-        del lane, kv, m
+        del dlane, lane, kv, m
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
     Path(a.out).write_text(json.dumps(results, indent=1))
 

@@ -49,19 +49,39 @@ def _port():
     return p
 
 
-def test_bench_torchrun_gloo_two_ranks(built_lib):
-    env = dict(os.environ, BENCH_BACKEND="gloo", PYTHONPATH=str(ROOT))
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+def _torchrun_bench(n, extra):
+    env = dict(os.environ, PYTHONPATH=str(ROOT))
+    env.pop("BENCH_BACKEND", None)  # the harness defaults to gloo (sessions exchange nothing)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"),
-           "--gpus", "2", "--steps", "1", "--warmup", "1", "--sim-clock", "--no-cpu"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+           "--gpus", str(n), "--steps", "1", "--warmup", "1", "--sim-clock", "--no-cpu", *extra]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
-    assert len(lines) == 1, r.stdout
-    d = json.loads(lines[0])
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+def test_bench_torchrun_gloo_two_ranks(built_lib):
+    d = _torchrun_bench(2, [])
     assert d["n_gpus"] == 2 and d["scaling"] == "weak"
-    assert d["latency_ms"]["sessions"] == 16  # 8 agents per rank, both ranks counted
+    assert d["config"]["config"] == "C3"
+    assert d["latency_ms"]["sessions"] == 64  # 32 agents per rank, both ranks counted
     assert d["value"] > 0
+    # both policies of the same episodes in one line, pooled over ranks
+    assert set(d["policies"]) == {"agentserve", "mixed_fcfs"}
+    assert d["policies"]["mixed_fcfs"]["sessions"] == 64
+    assert d["tails_vs_mixed_fcfs"]["tpot_p99"] is not None
+
+
+def test_bench_torchrun_gloo_eight_ranks_c5(built_lib):
+    """C5: Llama-3.1-8B-shaped, 64 agents per GPU as session-sharded replicas; world size 8 on
+    gloo (the driver's 8-GPU scaling launch), whole-job aggregation on rank 0."""
+    d = _torchrun_bench(8, ["--config", "c5", "--compare", "none"])
+    assert d["n_gpus"] == 8 and d["config"]["config"] == "C5"
+    assert d["config"]["agents_per_gpu"] == 64
+    assert d["latency_ms"]["sessions"] == 512
+    assert d["value"] > 0 and d["policies"]["agentserve"]["tpot_gaps"] > 0
 
 
 @pytest.mark.parametrize("env,want", [
