@@ -9,7 +9,7 @@
  *                      plus the device paged KV pool it now owns (block tables, append).
  *   asb_forward /
  *   asb_decode_launch <- decode_step_duration_ms   (/root/reference/proj/src/executor.hpp:76-77,
- *                      executor.cpp:207-220): one continuous-batching decode step, B single-token
+ *                      executor.cpp:84-97): one continuous-batching decode step, B single-token
  *                      rows + <= resume_chunk_tokens rows of an admitted resume
  *                      (engine.cpp:295-339).
  *   asb_prefill_launch <- prefill rate x length     (/root/reference/proj/src/engine.cpp:442-477).
@@ -76,7 +76,7 @@ asb_status asb_kv_create(asb_model* m, int num_blocks, asb_kv** out);
 void asb_kv_free(asb_kv* kv);
 int asb_kv_block_tokens(void);
 int asb_kv_free_blocks(const asb_kv* kv);
-/* reference registry protocol (executor.cpp:166-205) */
+/* reference registry protocol (executor.cpp:43-82) */
 asb_status asb_kv_begin_write(asb_kv* kv, uint32_t session);
 asb_status asb_kv_commit(asb_kv* kv, uint32_t session, int new_prefix);
 asb_status asb_kv_append(asb_kv* kv, uint32_t session, int tokens);

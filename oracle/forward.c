@@ -7,7 +7,7 @@
  *
  * PARITY STATUS: the reference (/root/reference/proj, agentsim) contains NO forward pass:
  * SPEC.md:9 lists "actual model inference and KV tensors" as out of scope and the simulator
- * replaces the forward with decode_step_duration_ms (src/executor.cpp:207-220) and a prefill
+ * replaces the forward with decode_step_duration_ms (src/executor.cpp:84-97) and a prefill
  * rate (src/engine.cpp:450-475).  The paper's real system extended llama.cpp,
  * which is not vendored and has no pinned version.  Logits / greedy ids / KV VALUES are
  * therefore "parity unpinned" against the reference: this file restates public Llama-3 /

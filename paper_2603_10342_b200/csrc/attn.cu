@@ -8,7 +8,7 @@
 //   K/V blocks arrive by TMA straight from the paged pool, softmax is one thread per
 //   query row (the TMEM lane it owns).  Replaces the prefill rate x length term of
 //   /root/reference/proj/src/engine.cpp:450-475 and the mu_R chunk term of
-//   /root/reference/proj/src/executor.cpp:216-218.
+//   /root/reference/proj/src/executor.cpp:93-95.
 // Decode attention (K2) lives in decode_attn.cu.
 #include <cuda.h>
 #include <cuda_runtime.h>

@@ -1,7 +1,7 @@
 // Paged decode attention (K2 in SURVEY §2.3) — one query token per decode row, the G query
 // heads of one KV head per CTA.  HBM-bound: each context token's K and V row is streamed
 // from HBM exactly once per (row, KV head).  Replaces the mu_D term of the reference's
-// decode_step_duration_ms (/root/reference/proj/src/executor.cpp:213-215).
+// decode_step_duration_ms (/root/reference/proj/src/executor.cpp:90-92).
 //
 // CTA = 1 producer warp + kWarps consumer warps, split-KV over gridDim.z:
 //   producer  : TMA (SWIZZLE_128B, evict-first) loads of 32-token K and V sub-blocks straight

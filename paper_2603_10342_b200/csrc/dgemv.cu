@@ -1,7 +1,7 @@
 // Small-batch decode linear layer ("dgemv"): Y[tok][n] = sum_k X[tok][k] * W[n][k] for
 // T <= 32 tokens, the regime of the decode steps at C1/C2 (B <= 8 rows + a <= 16-token
 // admitted resume chunk).  Replaces, with decode_attention, the mu_D term of the
-// reference's decode_step_duration_ms (/root/reference/proj/src/executor.cpp:207-220).
+// reference's decode_step_duration_ms (/root/reference/proj/src/executor.cpp:84-97).
 //
 // At T <= 32 a linear layer is a pure weight stream: 2 bytes of W per 2*T flops.  The
 // tcgen05 kernel (gemm.cu) pays a TMEM allocation, an mbarrier ring, a TMA round trip and —

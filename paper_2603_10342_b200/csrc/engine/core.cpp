@@ -554,7 +554,7 @@ void Prefixes::need_sealed(uint32_t s) const {
 }
 
 // Virtual-clock decode step: B tokens at mu_D then the admitted chunk at mu_R
-// (executor.cpp:207-220).
+// (executor.cpp:84-97).
 double step_ms(const Profile& p, int sms, int batch, int chunk) {
     if (batch < 0 || chunk < 0 || (batch == 0 && chunk == 0))
         raise(Err::Invalid, "decode step needs at least one stream or an admitted chunk");

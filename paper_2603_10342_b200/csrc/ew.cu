@@ -1,7 +1,7 @@
 // HBM-bound elementwise / row kernels of the forward (K1 + K6 in SURVEY §2.3):
 //   weight init (counter-based splitmix64; bit-identical to oracle/forward.c),
 //   embedding gather, RMSNorm, RoPE + paged-KV append (the device half of
-//   KvCacheRegistry, /root/reference/proj/src/executor.cpp:166-205), greedy argmax.
+//   KvCacheRegistry, /root/reference/proj/src/executor.cpp:43-82), greedy argmax.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 

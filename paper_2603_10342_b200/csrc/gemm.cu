@@ -2,7 +2,7 @@
 //   Y[tok][n] = sum_k X[tok][k] * W[n][k]   (+ bias / + residual / SiLU·mul / fp32)
 //
 // Replaces the simulated cost terms of the reference's executor
-// (decode_step_duration_ms, /root/reference/proj/src/executor.cpp:207-220, and the
+// (decode_step_duration_ms, /root/reference/proj/src/executor.cpp:84-97, and the
 // prefill rate x length arithmetic, /root/reference/proj/src/engine.cpp:450-475).
 //
 // Structure (192 threads, one CTA per SM):

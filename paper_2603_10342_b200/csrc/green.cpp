@@ -1,6 +1,6 @@
 // Green Context slot manager (H1 in SURVEY §2.3) behind asb_slots_*.
 //
-// Replaces SlotSet (/root/reference/proj/src/executor.hpp:20-42, executor.cpp:132-164):
+// Replaces SlotSet (/root/reference/proj/src/executor.hpp:20-42, executor.cpp:9-41):
 // the paper pre-establishes one SM partition per reservation level at start-up and rebinds
 // the decode / prefill threads between them at run time (§3.3, "<50 us per
 // rebinding").  Here every level 1..levels-1 owns a (decode, prefill) pair of green

@@ -3,7 +3,7 @@
 // execution lanes and the ragged-batch SLM forward.
 //
 // The forward is the work the reference simulates at its two seams:
-//   decode step  -> decode_step_duration_ms   (/root/reference/proj/src/executor.cpp:207-220)
+//   decode step  -> decode_step_duration_ms   (/root/reference/proj/src/executor.cpp:84-97)
 //   prefill unit -> remaining / rate           (/root/reference/proj/src/engine.cpp:450-475)
 // Numerics contract (restated by oracle/forward.c): bf16 storage of x / h / qkv / q / k / v /
 // attn / act, fp32 accumulation, single rounding after bias / residual / SiLU·mul epilogues.

@@ -8,7 +8,7 @@ stream of that level; the last level is the full device) and we record
   cold_prefill   : one `cold_len`-token prompt             -> tokens/s = cold_len / forward time
   resume_prefill : `resume_len` tokens appended to a `resume_ctx` context -> tokens/s
 exactly the quantities the reference's cost model divides by (decode_step_duration_ms,
-executor.cpp:207-220; the prefill rate x length arithmetic, engine.cpp:450-475).  Curves are made
+executor.cpp:84-97; the prefill rate x length arithmetic, engine.cpp:450-475).  Curves are made
 non-decreasing (running max) because the reference validator requires it (profile.cpp:81-128).
 
     python -m paper_2603_10342_b200.profile_measure --model qwen2.5-0.5b --out profiles/b200_profile_qwen2.5-0.5b.json

@@ -13,7 +13,7 @@ workload.cpp:143-180); fixed lengths are ranges with min = max = mean.
 Calibration (SURVEY.md §7 "Hard parts"): the reference anchors the TPOT SLO to the isolated
 single-stream step times a factor 8 (calibrate_slo, /root/reference/proj/src/metrics.cpp:30-43)
 and sets theta_high = tau, theta_low = tau/2 (src/config.cpp:185-188), because its cost model
-makes a decode step linear in the batch (1000*B/mu_D, src/executor.cpp:207-220).  A real B200
+makes a decode step linear in the batch (1000*B/mu_D, src/executor.cpp:84-97).  A real B200
 decode step is affine and nearly flat in B (weights + KV over HBM), so that tau is unattainable
 at any real batch and the controller saturates.  In wall-clock mode the thresholds are instead
 derived from the measured curve at the batch it was measured at (the profile's `measured`

@@ -1,6 +1,6 @@
 """Device KV registry and paged block tables (asb_kv_*).
 
-The protocol restates KvCacheRegistry (/root/reference/proj/src/executor.cpp:166-205) and
+The protocol restates KvCacheRegistry (/root/reference/proj/src/executor.cpp:43-82) and
 must behave exactly like its own test (/root/reference/proj/tests/test_executor.cpp:53-75):
 sealed / unsealed transitions, prefix growth, PROTOCOL on a read of an unsealed session and on
 a shrinking commit.  Block tables are integer state and must be bit-exact and deterministic:
