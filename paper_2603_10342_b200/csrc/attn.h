@@ -68,16 +68,16 @@ cudaError_t prefill_attention(const CUtensorMap& tmap_q, const CUtensorMap& tmap
                               __nv_bfloat16* out, float* part_o, float* part_ml, const AttnShape& s,
                               cudaStream_t stream);
 
-// Split-KV paged decode attention.  tmap_k32 / tmap_v32: the pool maps with 32-row boxes.
+// Split-KV paged decode attention.  tmap_kv: the pool as (col, row, half, K|V, page) with a
+// box of one whole block (64 rows x hd, K and V) -- make_tmap_kv_sub(.., box_rows = 64).
 // part_* workspaces are sized by the caller for n_items * hq * max_splits entries.
 // counters: [n_items][hkv] zero-initialised ints; the last split CTA of each (row, kv head)
 // merges the partials itself and resets its counter (no combine launch).
-cudaError_t decode_attention(const CUtensorMap& tmap_k32, const CUtensorMap& tmap_v32,
-                             const __nv_bfloat16* q, const DecodeItem* items, int n_items,
-                             int max_ctx, const int32_t* tables, __nv_bfloat16* out,
+cudaError_t decode_attention(const CUtensorMap& tmap_kv, const __nv_bfloat16* q, const DecodeItem* items,
+                             int n_items, int max_ctx, const int32_t* tables, __nv_bfloat16* out,
                              float* part_o, float* part_ml, int* counters, int max_splits, int num_sms,
                              const AttnShape& s, cudaStream_t stream);
 
-int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits, int ctas_per_sm, int warps);
+int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits);
 
 }  // namespace asb

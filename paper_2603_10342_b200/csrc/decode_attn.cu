@@ -3,21 +3,28 @@
 // from HBM exactly once per (row, KV head).  Replaces the mu_D term of the reference's
 // decode_step_duration_ms (/root/reference/proj/src/executor.cpp:90-92).
 //
-// CTA = 1 producer warp + kWarps consumer warps, split-KV over gridDim.z:
-//   producer  : TMA (SWIZZLE_128B, evict-first) loads of 32-token K and V sub-blocks straight
-//               from the paged pool into a kStages-deep smem ring, completion on mbarriers
-//   consumers : each warp owns whole sub-blocks (no CTA-wide barrier per block).  The G <= 8
-//               heads are the M rows of a warp-level bf16 tensor-core tile (m16n8k16):
-//                 S = Q . K^T   (B fragments by ldmatrix from the swizzled K tile)
-//                 online softmax on the S fragments (quad shuffles, per-warp m / l)
-//                 O += P . V    (P re-packed from the S fragments in registers, V fragments
-//                                by ldmatrix.trans)
-//               ~230 instructions per 32-key sub-block for all heads at once, so the kernel
-//               stays bandwidth-bound.  (tcgen05 needs M >= 64 — >= 8x wasted rows for
-//               G <= 8 — and a TMEM round trip per block; a register-resident warp MMA is
-//               the better fit for this memory-bound shape.)
-//   epilogue  : warps merge (m, l, O) through smem; the CTA writes bf16 output (one split)
-//               or fp32 partials merged by decode_combine_kernel.
+// CTA = 1 producer warp + 4 consumer warps, two CTAs per SM, split-KV over gridDim.z:
+//   producer  : ONE TMA request per 64-token KV block: the block's K page and V page are
+//               adjacent in the pool (attn.h), so a 5-D box (col, row, half, K|V, page) moves
+//               both as a single 32 KiB (hd 128) / 16 KiB (hd 64) SWIZZLE_128B copy into a
+//               3-stage (hd 128) / 6-stage ring, evict-first.  The per-SM TMA issue rate caps
+//               small requests (~7.5 M requests/s per SM: 4 KiB boxes -> ~60 GB/s/SM, 32 KiB
+//               -> ~175 GB/s/SM, profiles/r2_partition_probe.txt), which is what bounds decode
+//               on a 16-64 SM Green Context partition, where HBM itself is not the limit.
+//   consumers : all four warps share each stage, 16 keys each.  Keys are the M rows of a
+//               warp-level bf16 MMA (m16n8k16) and the G <= 8 heads its N columns, so no MMA
+//               row is padding:
+//                 S^T = K . Q^T          (A = K by ldmatrix, B = Q^T held in registers)
+//                 online softmax per head column (3 shuffles per head pair for the max; the
+//                 running sum stays per-thread until the end)
+//                 O^T += V^T . P^T       (A = V^T by ldmatrix.trans, B = P^T by movmatrix.trans
+//                                        of the S^T fragments)
+//               16 MMAs and 16 ldmatrix per warp per 64-token block.  (tcgen05 needs M >= 64
+//               and a TMEM round trip per block; a register-resident warp MMA is the better fit
+//               for this memory-bound shape.)
+//   epilogue  : warps merge (m, l, O) through smem; the CTA writes bf16 output (one split),
+//               or the splits of a (row, kv head) merge over DSMEM in a cluster / through fp32
+//               partials.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -34,50 +41,55 @@ namespace asb {
 
 namespace {
 
-constexpr int kSub = 32;   // tokens per streamed sub-block (half a KV block)
-constexpr int kWarps = 4;  // consumer warps per CTA (two CTAs per SM, see DC::kStages)
+constexpr int kWarps = 4;  // consumer warps per CTA, 16 keys of each 64-token block apiece
 constexpr int kThreadsD = (kWarps + 1) * 32;
 
 template <int HD>
 struct DC {
-    static constexpr int kHalves = HD / 64;                // 64-column SW128 boxes per row
-    static constexpr int kTile = kSub * HD * 2;            // one K (or V) sub-block, bytes
-    static constexpr int kStage = 2 * kTile;
-    // One stage per consumer warp (HD=128: 64 KB ring + 16 KB merge) or two (HD=64): two
-    // CTAs per SM, i.e. 8 consumer warps and 128 KB of K/V in flight per SM.  Measured best
-    // of the (warps, stages) sweep in profiles/r1_decode_attn_sweep.txt.
-    static constexpr int kStages = HD == 128 ? 4 : 8;
+    static constexpr int kStage = 2 * kBlockTokens * HD * 2;   // K page + V page of one block
+    // 96 KiB of K/V in flight per CTA, two CTAs per SM (192 KiB per SM)
+    static constexpr int kStages = HD == 128 ? 3 : 6;
     static constexpr int kRing = kStages * kStage;
 };
 
-// Stage of item i.  Item i is consumed by warp i % W; giving every warp its own S / W stages
-// (visited in order) means each mbarrier has exactly one waiter that waits its phases
-// strictly in sequence — with round-robin consumers sharing a ring, a fast warp could wait
-// for phase k+2 of a stage while phase k+1 is still pending, and the parity-based wait would
-// alias and return early.
-__device__ __forceinline__ int stage_of(int i, int W, int S) { return (i % W) + W * ((i / W) % (S / W)); }
+// transpose an 8x8 bf16 matrix held one row-pair per thread (the mma / ldmatrix fragment)
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+
+// byte offset of 16-byte chunk c (0..HD/8-1) of row r (0..63) of the K (kv = 0) or V (kv = 1)
+// page in a stage: the box lands as [K|V][half][64 rows][128 B] and SWIZZLE_128B XORs the
+// chunk with the 128-byte line index mod 8 (= r mod 8)
+template <int HD>
+__device__ __forceinline__ uint32_t kv_off(int kv, int r, int c) {
+    constexpr int H = HD / 64;
+    const int line = ((kv * H + (c >> 3)) * kBlockTokens) + r;
+    return line * 128 + (((c & 7) ^ (r & 7)) << 4);
+}
 
 template <int HD>
 __global__ void __launch_bounds__(kThreadsD, 2)
-    decode_attn_kernel(const __grid_constant__ CUtensorMap tmap_k,
-                       const __grid_constant__ CUtensorMap tmap_v,
+    decode_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv,
                        const __nv_bfloat16* __restrict__ q, const DecodeItem* __restrict__ items,
                        const int32_t* __restrict__ tables, __nv_bfloat16* __restrict__ out,
                        float* __restrict__ part_o, float* __restrict__ part_ml,
-                       int* __restrict__ counters, int subs_per_split, int n_stages, int cluster_merge,
+                       int* __restrict__ counters, int pages_per_split, int cluster_merge,
                        AttnShape s) {
     using C = DC<HD>;
-    constexpr int NT = HD / 8;  // O n-tiles (8 dims each)
-    const int kWarpsR = blockDim.x / 32 - 1;  // consumer warps
-    const int kStagesR = n_stages;
+    constexpr int MT = HD / 16;  // O^T m-tiles (16 dims each)
+    constexpr int kStagesR = C::kStages;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
     uint8_t* ring = smem;
-    float* mrg = reinterpret_cast<float*>(smem + kStagesR * C::kStage);  // [warp][8][HD]
-    float* mls = mrg + kWarpsR * 8 * HD;                                 // [warp][8][2]
-    uint64_t* full = reinterpret_cast<uint64_t*>(mls + kWarpsR * 16);
+    // after the ring drains: per-warp O^T [warp][8 heads][HD] at its start (merge), the
+    // cluster-merge record behind it
+    float* mrg = reinterpret_cast<float*>(ring);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kRing);
     uint64_t* empty = full + kStagesR;
+    float* mls = reinterpret_cast<float*>(empty + kStagesR);  // [warp][8][2]
 
     const int cta_id = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     auto stamp = [&](int k) {
@@ -92,50 +104,41 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     const int kvh = blockIdx.y;
     const int G = s.hq / s.hkv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_sub = (it.ctx_len + kSub - 1) / kSub;
-    const int s0 = blockIdx.z * subs_per_split;
-    const int n_local = max(0, min(n_sub, s0 + subs_per_split) - s0);
+    const int n_pages = (it.ctx_len + kBlockTokens - 1) / kBlockTokens;
+    const int p0 = blockIdx.z * pages_per_split;
+    const int n_local = max(0, min(n_pages, p0 + pages_per_split) - p0);
     const int32_t* table = tables + it.table_off;
 
     if (threadIdx.x == 0) {
-        tma_prefetch_desc(&tmap_k);
-        tma_prefetch_desc(&tmap_v);
+        tma_prefetch_desc(&tmap_kv);
         for (int i = 0; i < kStagesR; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+            mbar_init(&empty[i], kWarps);
         }
         fence_barrier_init();
     }
     __syncthreads();
     pdl_trigger();
 
-    if (warp == kWarpsR) {
+    if (warp == kWarps) {
         // ------------------------------------------------------------ producer
         // K/V of positions before this step's token were written by earlier steps: stream them
         // while the kernel before us (the QKV projection appending the new token) is still
-        // running, and wait for it only before the sub-block that holds the new token.
+        // running, and wait for it only before the block that holds the new token.
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            const int new_sub = (it.ctx_len - 1) / kSub;
+            const int new_page = (it.ctx_len - 1) / kBlockTokens;
             bool waited = false;
             for (int i = 0; i < n_local; ++i) {
-                if (!waited && s0 + i >= new_sub) {
+                if (!waited && p0 + i >= new_page) {
                     pdl_wait();
                     waited = true;
                 }
-                const int st = stage_of(i, kWarpsR, kStagesR);
+                const int st = i % kStagesR;
                 mbar_wait(&empty[st], ((i / kStagesR) & 1) ^ 1);
                 mbar_expect_tx(&full[st], C::kStage);
-                const int j = s0 + i;
-                const int blk = table[j >> 1];
-                const int row = ((s.layer * s.num_blocks + blk) * s.hkv + kvh) * kKvPageRows + (j & 1) * kSub;
-                uint8_t* kd = ring + st * C::kStage;
-                uint8_t* vd = kd + C::kTile;
-#pragma unroll
-                for (int h = 0; h < C::kHalves; ++h) {
-                    tma_load_2d_hint(kd + h * (kSub * 128), &tmap_k, &full[st], h * 64, row, pol);
-                    tma_load_2d_hint(vd + h * (kSub * 128), &tmap_v, &full[st], h * 64, row, pol);
-                }
+                const int page = (s.layer * s.num_blocks + table[p0 + i]) * s.hkv + kvh;
+                tma_load_5d_hint(ring + st * C::kStage, &tmap_kv, &full[st], 0, 0, 0, 0, page, pol);
             }
             if (!waited) pdl_wait();
         }
@@ -146,135 +149,139 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     pdl_wait();  // q comes from the kernel before us
     if (threadIdx.x == 0) stamp(1);
     const int g = lane >> 2, t = lane & 3;  // fragment row / column-pair owner
-    // Q A-fragments (rows = heads): (row g, k 2t..2t+1) and (row g, k 2t+8..2t+9); the
-    // fragment registers of rows g+8 and of rows >= G are zero
-    uint32_t qa[HD / 16][2];
+    const int kw = warp * 16;               // this warp's keys within each block
+    // Q^T B-fragments (k = dims, n = heads): head g, dims (2t, 2t+1) and (2t+8, 2t+9) of each
+    // 16-dim k-step; heads >= G are zero columns
+    uint32_t qb[HD / 16][2];
     {
         const __nv_bfloat16* qrow = q + (size_t)it.q_row * s.hq * HD + (size_t)(kvh * G + g) * HD;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
             if (g < G) {
-                qa[kk][0] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t);
-                qa[kk][1] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t + 8);
+                qb[kk][0] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t);
+                qb[kk][1] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t + 8);
             } else {
-                qa[kk][0] = qa[kk][1] = 0u;
+                qb[kk][0] = qb[kk][1] = 0u;
             }
         }
     }
-    float o[NT][4];
+    // O^T accumulators: m-tile mt holds (dim mt*16+g, heads 2t, 2t+1) and (dim +8, same heads)
+    float o[MT][4];
 #pragma unroll
-    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-    float m_run = -FLT_MAX, l_run = 0.f;
+    for (int n = 0; n < MT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_run[2] = {-FLT_MAX, -FLT_MAX}, l_run[2] = {0.f, 0.f};  // heads 2t, 2t+1
+    const int mi = lane >> 3;
 
-    for (int i = warp; i < n_local; i += kWarpsR) {
-        const int st = stage_of(i, kWarpsR, kStagesR);
+    for (int i = 0; i < n_local; ++i) {
+        const int st = i % kStagesR;
         mbar_wait(&full[st], (i / kStagesR) & 1);
-        if (i == 0 && lane == 0) stamp(2);
+        if (i == 0 && threadIdx.x == 0) stamp(2);
         if (s.dbg_load_only) {  // timing ablation (ASB_DEBUG_SKIP=attnmath): the load stream alone
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
             continue;
         }
-        const uint32_t kt = smem_u32(ring + st * C::kStage);
-        const uint32_t vt = kt + C::kTile;
-        // ---- S = Q K^T : 4 n-tiles of 8 keys
-        float sacc[4][4];
+        const uint32_t base = smem_u32(ring + st * C::kStage);
+        // ---- S^T = K . Q^T : 16 keys x 8 heads, two accumulation chains over the dims
+        float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+        {
+            const int key = kw + (mi & 1) * 8 + (lane & 7);
 #pragma unroll
-        for (int n = 0; n < 4; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-#pragma unroll
-            for (int np = 0; np < 2; ++np) {  // pairs of key n-tiles
-                // matrices: (ntile 2np, k lo), (2np, k hi), (2np+1, k lo), (2np+1, k hi)
-                const int mi = lane >> 3;
-                const int key = (2 * np + (mi >> 1)) * 8 + (lane & 7);
-                const int chunk = 2 * kk + (mi & 1);
-                uint32_t b0, b1, b2, b3;
-                ldsm_x4(kt + sw_off<HD>(key, chunk), b0, b1, b2, b3);
-                mma16816(sacc[2 * np], qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
-                mma16816(sacc[2 * np + 1], qa[kk][0], 0u, qa[kk][1], 0u, b2, b3);
+            for (int kk = 0; kk < HD / 16; ++kk) {
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4(base + kv_off<HD>(0, key, 2 * kk + (mi >> 1)), a0, a1, a2, a3);
+                if (kk & 1) mma16816(sb, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+                else mma16816(sa, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
             }
         }
-        // ---- online softmax on row g (keys 8n + 2t + {0,1})
-        const int kbase = (s0 + i) * kSub;
-        float mx = m_run;
+        // ---- online softmax per head column: values (key g | g+8, head 2t + j)
+        const int kbase = (p0 + i) * kBlockTokens + kw;
+        const bool ok0 = kbase + g < it.ctx_len, ok1 = kbase + g + 8 < it.ctx_len;
+        float sv[4];
 #pragma unroll
-        for (int n = 0; n < 4; ++n)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const bool ok = kbase + 8 * n + 2 * t + e < it.ctx_len;
-                sacc[n][e] = ok ? sacc[n][e] * s.scale_log2 : -FLT_MAX;
-                mx = fmaxf(mx, sacc[n][e]);
-            }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float alpha = exp2f(m_run - mx);
-        float psum = 0.f;
-        uint32_t pa[2][2];  // P A-fragments for the two 16-key k-steps (row g)
-#pragma unroll
-        for (int n = 0; n < 4; ++n) {
-            const float p0 = sacc[n][0] == -FLT_MAX ? 0.f : exp2f(sacc[n][0] - mx);
-            const float p1 = sacc[n][1] == -FLT_MAX ? 0.f : exp2f(sacc[n][1] - mx);
-            const uint32_t pk = pack_bf16(p0, p1);
-            psum += bf16_lo(pk) + bf16_hi(pk);  // sum what P.V will actually use
-            pa[n >> 1][n & 1] = pk;
+        for (int e = 0; e < 4; ++e) {
+            const bool ok = e < 2 ? ok0 : ok1;
+            sv[e] = ok ? (sa[e] + sb[e]) * s.scale_log2 : -FLT_MAX;
         }
-        psum += __shfl_xor_sync(0xffffffffu, psum, 1);
-        psum += __shfl_xor_sync(0xffffffffu, psum, 2);
-        l_run = l_run * alpha + psum;
-        m_run = mx;
+        float alpha[2], mx[2];
 #pragma unroll
-        for (int n = 0; n < NT; ++n) {
-            o[n][0] *= alpha;
-            o[n][1] *= alpha;
+        for (int j = 0; j < 2; ++j) {
+            float m = fmaxf(m_run[j], fmaxf(sv[j], sv[2 + j]));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+            mx[j] = m;
+            alpha[j] = exp2f(m_run[j] - m);
+            m_run[j] = m;
         }
-        // ---- O += P V : 2 k-steps of 16 keys x NT n-tiles of 8 dims
+        float p[4];
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
+        for (int e = 0; e < 4; ++e) p[e] = sv[e] == -FLT_MAX ? 0.f : exp2f(sv[e] - mx[e & 1]);
+        const uint32_t p01 = pack_bf16(p[0], p[1]), p23 = pack_bf16(p[2], p[3]);
+        // sum what P.V will actually use (the bf16-rounded weights)
+        l_run[0] = l_run[0] * alpha[0] + (bf16_lo(p01) + bf16_lo(p23));
+        l_run[1] = l_run[1] * alpha[1] + (bf16_hi(p01) + bf16_hi(p23));
+        // P^T B-fragments: (keys 2t, 2t+1 | 2t+8, 2t+9; head g)
+        const uint32_t b0 = movmatrix_t(p01), b1 = movmatrix_t(p23);
+        // ---- O^T = alpha O^T + V^T . P^T : MT m-tiles of 16 dims
+        {
+            const int key = kw + (mi >> 1) * 8 + (lane & 7);
 #pragma unroll
-            for (int dp = 0; dp < NT / 2; ++dp) {  // pairs of dim n-tiles
-                const int mi = lane >> 3;
-                const int key = ks * 16 + (mi & 1) * 8 + (lane & 7);
-                const int chunk = 2 * dp + (mi >> 1);
-                uint32_t b0, b1, b2, b3;
-                ldsm_x4_t(vt + sw_off<HD>(key, chunk), b0, b1, b2, b3);
-                mma16816(o[2 * dp], pa[ks][0], 0u, pa[ks][1], 0u, b0, b1);
-                mma16816(o[2 * dp + 1], pa[ks][0], 0u, pa[ks][1], 0u, b2, b3);
+            for (int mt = 0; mt < MT; ++mt) {
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4_t(base + kv_off<HD>(1, key, 2 * mt + (mi & 1)), a0, a1, a2, a3);
+                o[mt][0] *= alpha[0];
+                o[mt][1] *= alpha[1];
+                o[mt][2] *= alpha[0];
+                o[mt][3] *= alpha[1];
+                mma16816(o[mt], a0, a1, a2, a3, b0, b1);
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
     }
+    // per-thread partial sums -> the head's sum over this warp's keys
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        l_run[j] += __shfl_xor_sync(0xffffffffu, l_run[j], 4);
+        l_run[j] += __shfl_xor_sync(0xffffffffu, l_run[j], 8);
+        l_run[j] += __shfl_xor_sync(0xffffffffu, l_run[j], 16);
+    }
 
     // ---------------------------------------------------------------- merge warps
     if (threadIdx.x == 0) stamp(3);
+    named_sync(1, kWarps * 32);  // every warp is done with the ring: it becomes merge space
     float* mw = mrg + warp * 8 * HD;
-    if (g < G) {
 #pragma unroll
-        for (int n = 0; n < NT; ++n) {
-            mw[g * HD + n * 8 + 2 * t] = o[n][0];
-            mw[g * HD + n * 8 + 2 * t + 1] = o[n][1];
-        }
-        if (t == 0) {
-            mls[(warp * 8 + g) * 2] = m_run;
-            mls[(warp * 8 + g) * 2 + 1] = l_run;
+    for (int j = 0; j < 2; ++j) {
+        const int h = 2 * t + j;
+        if (h < G) {
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                mw[h * HD + mt * 16 + g] = o[mt][j];
+                mw[h * HD + mt * 16 + g + 8] = o[mt][2 + j];
+            }
+            if (g == 0) {
+                mls[(warp * 8 + h) * 2] = m_run[j];
+                mls[(warp * 8 + h) * 2 + 1] = l_run[j];
+            }
         }
     }
-    named_sync(1, kWarpsR * 32);
+    named_sync(1, kWarps * 32);
     const bool single = gridDim.z == 1;
     const bool cmerge = !single && cluster_merge;
     // cluster merge: this CTA's (M, L, O) parked at the start of the drained ring
-    float* cO = reinterpret_cast<float*>(ring);  // [G][HD]
+    float* cO = mrg + kWarps * 8 * HD;           // [G][HD], behind the warp records
     float* cM = cO + 8 * HD;                     // [G]
     float* cL = cM + 8;                          // [G]
-    for (int e = threadIdx.x; e < G * HD; e += kWarpsR * 32) {
+    for (int e = threadIdx.x; e < G * HD; e += kWarps * 32) {
         const int h = e / HD, d = e % HD;
         float M = -FLT_MAX;
 #pragma unroll
-        for (int w = 0; w < kWarpsR; ++w) M = fmaxf(M, mls[(w * 8 + h) * 2]);
+        for (int w = 0; w < kWarps; ++w) M = fmaxf(M, mls[(w * 8 + h) * 2]);
         float L = 0.f, O = 0.f;
 #pragma unroll
-        for (int w = 0; w < kWarpsR; ++w) {
+        for (int w = 0; w < kWarps; ++w) {
             const float lw = mls[(w * 8 + h) * 2 + 1];
             if (lw == 0.f) continue;
             const float f = exp2f(mls[(w * 8 + h) * 2] - M);
@@ -314,7 +321,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         const int S = gridDim.z, r = blockIdx.z;
         const int n = G * HD, lo = (n * r) / S, hi = (n * (r + 1)) / S;
         const uint32_t bO = smem_u32(cO), bM = smem_u32(cM), bL = smem_u32(cL);
-        for (int e = lo + threadIdx.x; e < hi; e += kWarpsR * 32) {
+        for (int e = lo + threadIdx.x; e < hi; e += kWarps * 32) {
             const int h = e / HD, d = e % HD;
             float mq[8], lq[8], oq[8];
 #pragma unroll
@@ -348,14 +355,14 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     // arithmetic as decode_combine_kernel: deterministic), then re-arms the counter.
     __shared__ int last_s;
     __threadfence();
-    named_sync(1, kWarpsR * 32);
+    named_sync(1, kWarps * 32);
     if (threadIdx.x == 0) {
         int* cnt = counters + blockIdx.x * gridDim.y + kvh;
         const int prev = atomicAdd(cnt, 1);
         last_s = prev == static_cast<int>(gridDim.z) - 1;
         if (last_s) *cnt = 0;
     }
-    named_sync(1, kWarpsR * 32);
+    named_sync(1, kWarps * 32);
     if (threadIdx.x == 0) stamp(4);
     if (!last_s) return;
     __threadfence();
@@ -365,13 +372,13 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     float* wsp = reinterpret_cast<float*>(smem);  // [G][splits]
     float* linv = wsp + 8 * splits;               // [G]
     float* lsp = linv + 8;  // [G][splits] l
-    for (int i = threadIdx.x; i < G * splits; i += kWarpsR * 32) {  // all (m, l) loads at once
+    for (int i = threadIdx.x; i < G * splits; i += kWarps * 32) {  // all (m, l) loads at once
         const int h = i / splits, sp = i % splits;
         const size_t sl = ((size_t)blockIdx.x * s.hq + kvh * G + h) * splits + sp;
         wsp[i] = __ldcg(part_ml + sl * 2);
         lsp[i] = __ldcg(part_ml + sl * 2 + 1);
     }
-    named_sync(1, kWarpsR * 32);
+    named_sync(1, kWarps * 32);
     if (threadIdx.x < G) {
         float M = -FLT_MAX;
         for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, wsp[threadIdx.x * splits + sp]);
@@ -384,8 +391,8 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         }
         linv[threadIdx.x] = L;
     }
-    named_sync(1, kWarpsR * 32);
-    for (int e = threadIdx.x; e < G * HD; e += kWarpsR * 32) {
+    named_sync(1, kWarps * 32);
+    for (int e = threadIdx.x; e < G * HD; e += kWarps * 32) {
         const int h = e / HD, d = e % HD;
         const int hh = kvh * G + h;
         const float* po = part_o + ((size_t)blockIdx.x * s.hq + hh) * splits * HD + d;
@@ -428,18 +435,14 @@ __global__ void decode_combine_kernel(const DecodeItem* __restrict__ items,
 }
 
 template <int HD>
-cudaError_t launch_hd(const CUtensorMap& tk, const CUtensorMap& tv, const __nv_bfloat16* q,
-                      const DecodeItem* items, int n_items, int splits, int sps, const int32_t* tables,
-                      __nv_bfloat16* out, float* po, float* pml, int* cnt, const AttnShape& s, cudaStream_t st) {
+cudaError_t launch_hd(const CUtensorMap& tkv, const __nv_bfloat16* q, const DecodeItem* items, int n_items,
+                      int splits, int pps, const int32_t* tables, __nv_bfloat16* out, float* po, float* pml,
+                      int* cnt, const AttnShape& s, cudaStream_t st) {
     using C = DC<HD>;
-    static const int warps = std::getenv("ASB_DECODE_WARPS") ? std::atoi(std::getenv("ASB_DECODE_WARPS")) : kWarps;
-    static const int stages0 = std::getenv("ASB_DECODE_STAGES") ? std::atoi(std::getenv("ASB_DECODE_STAGES")) : C::kStages;
-    static const int stages = std::max(warps, (stages0 / warps) * warps);  // multiple of warps
-    const int smem = stages * C::kStage + warps * 8 * HD * 4 + warps * 16 * 4 + 2 * stages * 8 + 1024;
+    const int smem = C::kRing + 2 * C::kStages * 8 + kWarps * 16 * 4 + 1024;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024);
+        cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -451,7 +454,7 @@ cudaError_t launch_hd(const CUtensorMap& tk, const CUtensorMap& tv, const __nv_b
     if (cmerge) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
-        cfg.blockDim = dim3((warps + 1) * 32);
+        cfg.blockDim = dim3(kThreadsD);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute a[2];
@@ -467,12 +470,11 @@ cudaError_t launch_hd(const CUtensorMap& tk, const CUtensorMap& tv, const __nv_b
         }
         cfg.attrs = a;
         cfg.numAttrs = na;
-        e = cudaLaunchKernelEx(&cfg, decode_attn_kernel<HD>, tk, tv, q, items, tables, out, po, pml, cnt, sps,
-                               stages, cmerge, s);
-        return e;
+        return cudaLaunchKernelEx(&cfg, decode_attn_kernel<HD>, tkv, q, items, tables, out, po, pml, cnt, pps,
+                                  cmerge, s);
     }
-    e = launch_k(decode_attn_kernel<HD>, grid, dim3((warps + 1) * 32), smem, st, tk, tv, q, items,
-                 tables, out, po, pml, cnt, sps, stages, 0, s);
+    e = launch_k(decode_attn_kernel<HD>, grid, dim3(kThreadsD), smem, st, tkv, q, items, tables, out, po, pml,
+                 cnt, pps, 0, s);
     if (e == cudaSuccess && splits > 1 && !cnt)
         e = launch_k(decode_combine_kernel<HD>, dim3(n_items, s.hq), dim3(HD), 0, st, items,
                      static_cast<const float*>(po), static_cast<const float*>(pml), splits, out, s.hq);
@@ -488,11 +490,11 @@ int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits
     // (C3 73% -> 84%, C4 84% -> 92% of HBM peak on the full device); on a Green Context
     // partition it also avoids ragged second waves (128 (row, head) items on a 48-SM
     // partition: 1 split = 2 waves of full items, 3 splits = 4 waves of 1/3 items = 1.33).
-    // >= 2 sub-blocks per consumer warp.
-    const int subs = (max_ctx + kSub - 1) / kSub;
+    // >= 3 blocks (192 keys) per split.
+    const int pages = (max_ctx + kBlockTokens - 1) / kBlockTokens;
     const int base = std::max(n_items * hkv, 1);
     const int slots = 2 * std::max(num_sms, 1);
-    const int cap = std::max(1, std::min(max_splits, subs / (2 * kWarps)));
+    const int cap = std::max(1, std::min(max_splits, pages / 3));
     int best = 1;
     double best_t = 1e30;
     for (int sp = 1; sp <= cap; ++sp) {
@@ -506,9 +508,8 @@ int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits
     return best;
 }
 
-cudaError_t decode_attention(const CUtensorMap& tmap_k32, const CUtensorMap& tmap_v32,
-                             const __nv_bfloat16* q, const DecodeItem* items, int n_items,
-                             int max_ctx, const int32_t* tables, __nv_bfloat16* out,
+cudaError_t decode_attention(const CUtensorMap& tmap_kv, const __nv_bfloat16* q, const DecodeItem* items,
+                             int n_items, int max_ctx, const int32_t* tables, __nv_bfloat16* out,
                              float* part_o, float* part_ml, int* counters, int max_splits, int num_sms,
                              const AttnShape& s, cudaStream_t stream) {
     if (n_items <= 0) return cudaSuccess;
@@ -519,15 +520,15 @@ cudaError_t decode_attention(const CUtensorMap& tmap_k32, const CUtensorMap& tma
     const int splits0 = force > 0 ? std::min(force, max_splits)  // partial buffers hold max_splits
                                   : decode_splits(n_items, s.hkv, max_ctx, num_sms,
                                                   no_cluster ? max_splits : std::min(max_splits, 8));
-    const int subs = (max_ctx + kSub - 1) / kSub;
-    const int sps = (subs + splits0 - 1) / splits0;
-    const int splits = (subs + sps - 1) / sps;
+    const int pages = (max_ctx + kBlockTokens - 1) / kBlockTokens;
+    const int pps = (pages + splits0 - 1) / splits0;
+    const int splits = (pages + pps - 1) / pps;
     if (s.hd == 128)
-        return launch_hd<128>(tmap_k32, tmap_v32, q, items, n_items, splits, sps, tables, out, part_o,
-                              part_ml, counters, s, stream);
+        return launch_hd<128>(tmap_kv, q, items, n_items, splits, pps, tables, out, part_o, part_ml, counters, s,
+                              stream);
     if (s.hd == 64)
-        return launch_hd<64>(tmap_k32, tmap_v32, q, items, n_items, splits, sps, tables, out, part_o,
-                             part_ml, counters, s, stream);
+        return launch_hd<64>(tmap_kv, q, items, n_items, splits, pps, tables, out, part_o, part_ml, counters, s,
+                             stream);
     return cudaErrorInvalidValue;
 }
 

@@ -236,7 +236,7 @@ struct asb_kv {
     __nv_bfloat16* pool = nullptr;  // interleaved K|V pages (attn.h)
     __nv_bfloat16 *k_pool = nullptr, *v_pool = nullptr;  // pool, pool + one page (element views)
     CUtensorMap tk, tv;      // box 64 rows (prefill attention)
-    CUtensorMap tk32, tv32;  // box 32 rows (decode attention sub-blocks)
+    CUtensorMap tkv;         // whole K|V block per box (decode attention)
     std::vector<int> free_list;  // LIFO: back() is handed out next
     struct Sess {
         std::vector<int32_t> blocks;
@@ -679,13 +679,12 @@ asb_status asb_kv_create(asb_model* m, int num_blocks, asb_kv** out) {
         kv->v_pool = kv->pool + size_t(kBlockTokens) * s.hd;
         const long rows = long(pages) * kKvPageRows;
         if (rows >= (1l << 31)) fail(ASB_ERR_VALIDATION, "KV pool too large for 32-bit TMA rows");
-        // [64 rows][64 cols] (prefill attention) and [32 rows][64 cols] (decode sub-blocks)
-        // boxes of the K pages (row = page*128 + t on the k_pool view) and the V pages (the
-        // same row index on the v_pool view, one page further)
+        // [64 rows][64 cols] boxes of the K pages (row = page*128 + t on the k_pool view) and the
+        // V pages (the same row index on the v_pool view, one page further) for prefill
+        // attention; one box per whole block, K and V together, for decode attention
         if (!make_tmap_bf16(&kv->tk, kv->k_pool, int(rows), s.hd, s.hd, kBlockTokens) ||
             !make_tmap_bf16(&kv->tv, kv->v_pool, int(rows - kBlockTokens), s.hd, s.hd, kBlockTokens) ||
-            !make_tmap_bf16(&kv->tk32, kv->k_pool, int(rows), s.hd, s.hd, 32) ||
-            !make_tmap_bf16(&kv->tv32, kv->v_pool, int(rows - kBlockTokens), s.hd, s.hd, 32))
+            !make_tmap_kv_sub(&kv->tkv, kv->pool, long(pages), s.hd, kBlockTokens, kBlockTokens))
             fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for the KV pool");
         kv->free_list.reserve(num_blocks);
         for (int b = num_blocks - 1; b >= 0; --b) kv->free_list.push_back(b);
@@ -1140,7 +1139,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                 }
                 if (!ditems.empty() && !skip("attn"))
                     L->timed(ASB_STAT_DECODE_ATTN, dattn_bytes, [&] {
-                        cuda_check(decode_attention(kv->tk32, kv->tv32, L->q, d_ditems, int(ditems.size()),
+                        cuda_check(decode_attention(kv->tkv, L->q, d_ditems, int(ditems.size()),
                                                     max_ctx, d_tbl, L->attn, L->part_o, L->part_ml,
                                                     L->dcnt, L->max_splits, L->n_sms(), as, st),
                                    "decode attention");
