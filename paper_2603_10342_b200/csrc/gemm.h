@@ -93,6 +93,36 @@ struct DgemvParams {
 int dgemv_max_tokens();
 cudaError_t dgemv_launch(DgemvParams p, int num_sms, cudaStream_t stream);
 
+// Decode linear on a TMA-fed smem ring + legacy warp MMAs (tgemv.cu), T <= 32 tokens: the
+// weight-streaming kernel for decode steps on Green Context partitions.  tmap_w: the weight's
+// packed map with a 2-k-block box (make_tmap_packed(.., 1, 2)); tmap_x: an activation k-pair
+// map with 32-row boxes (make_tmap_act_kpair(.., 32)).  Epilogue fields as in GemmParams
+// (EPI_QKV needs 128 % hd == 0).  splits: K split (0 = chosen for num_sms); ws / cnt: the
+// split partials [units][32][128] fp32 and per-tile arrival counters (zeroed, self-resetting).
+struct TgemvParams {
+    int T, n_out, K;
+    int tiles;   // 128-row weight tiles (rows_pad / 128)
+    int splits;  // 0: chosen by tgemv_launch
+    int kunits, kups;  // internal: 128-wide k-units, per split
+    int epi;
+    __nv_bfloat16* out;
+    float* out_f32;
+    int ldo;
+    const __nv_bfloat16* bias;
+    const __nv_bfloat16* resid;
+    int ldr;
+    RopeEpi rope;
+    unsigned long long* amax;
+    PostNorm post;
+    float* ws;
+    int* cnt;
+    int dbg_load_only;  // timing ablation (ASB_DEBUG_SKIP=tgmath): consumers release stages unread
+};
+int tgemv_max_tokens();
+int tgemv_splits(int tiles, int kunits, int num_sms);
+cudaError_t tgemv_launch(const CUtensorMap& tmap_w, const CUtensorMap& tmap_x, TgemvParams p, int num_sms,
+                         cudaStream_t stream);
+
 int gemm_pick_bn(int n);
 int gemm_smem_bytes(int bn);
 // Cluster split-K factor for a swap-path GEMM of `tiles` weight tiles: the largest S <= 8

@@ -272,11 +272,13 @@ struct asb_lane {
     float *logits, *part_o, *part_ml, *ppart_o, *ppart_ml;
     int* dcnt = nullptr;  // decode-attention split arrival counters [rows][hkv] (self-resetting)
     int* post_cnt = nullptr;  // grid arrival counter of the fused post-norm (self-resetting)
+    float* tg_ws = nullptr;   // tgemv split partials [4 * SMs units][32][128] fp32
+    int* tg_cnt = nullptr;    // tgemv per-tile split arrival counters (self-resetting)
     // split merge inside the decode-attention kernel (last-arriving split) instead of a
     // combine launch; ASB_ATTN_COMBINE=1 selects the separate combine kernel
     bool attn_fused_merge = std::getenv("ASB_ATTN_COMBINE") == nullptr;
     unsigned long long* attn_dbg = nullptr;  // ASB_ATTN_TIMELINE=1: decode-attention CTA stamps
-    CUtensorMap map_x[7];
+    CUtensorMap map_x[8];
     bool pdl = std::getenv("ASB_NO_PDL") == nullptr;  // programmatic dependent launch
     unsigned long long* dbg_times = nullptr;  // ASB_GEMM_TIMELINE: per-CTA stamps of the last GEMM
     size_t ppart_rows = 0;
@@ -287,7 +289,7 @@ struct asb_lane {
     size_t meta_ints = 0;
     std::vector<void*> allocs;
     // tensor maps of GEMM inputs: [0] box 128 (normal A), [1..4] box 32/64/128/256 (swap B)
-    CUtensorMap map_h[7], map_attn[7], map_act[7], map_hl[7], map_q;
+    CUtensorMap map_h[8], map_attn[8], map_act[8], map_hl[8], map_q;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t ev_switch = nullptr;  // orders a rebound stream after the old one (set_stream)
     bool launched = false;
@@ -364,14 +366,16 @@ struct asb_lane {
 namespace {
 
 // [0] box 128 rows (normal-path A), [1..4] box 32/64/128/256 (swap-path B), [5..6] k-pair
-// boxes of 32/64 rows (swap-path B with two k-blocks per stage)
-constexpr int kActMaps = 7;
+// boxes of 32/64 rows (swap-path B with two k-blocks per stage), [7] k-pair box of 16 rows
+// (tgemv at <= 16 tokens)
+constexpr int kActMaps = 8;
 void act_maps(CUtensorMap* maps, const void* base, int rows, int cols) {
     const int boxes[5] = {128, 32, 64, 128, 256};
     for (int i = 0; i < 5; ++i)
         if (!make_tmap_bf16(&maps[i], base, rows, cols, cols, boxes[i]))
             fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for an activation");
-    if (!make_tmap_act_kpair(&maps[5], base, rows, cols, 32) || !make_tmap_act_kpair(&maps[6], base, rows, cols, 64))
+    if (!make_tmap_act_kpair(&maps[5], base, rows, cols, 32) || !make_tmap_act_kpair(&maps[6], base, rows, cols, 64) ||
+        !make_tmap_act_kpair(&maps[7], base, rows, cols, 16))
         fail(ASB_ERR_CUDA, "cuTensorMapEncodeTiled failed for an activation (k-pair)");
 }
 
@@ -405,7 +409,35 @@ bool use_dgemv(int T, const Weight& w, int num_sms) {
     return !off && T <= 16 && num_sms > 32 && per_sm <= 160e3;
 }
 
-// Y[T][n_out] = X[T][k] . W^T with the path chosen by T (path 2 = dgemv, 1 = tcgen05
+// tgemv split workspace of a lane: units <= 4 waves of one CTA per SM (tgemv_splits)
+constexpr int kTgMaxUnits = 4 * 160;
+constexpr int kTgMaxTiles = 4096;
+void tgemv_buffers(asb_lane* L) {
+    if (L->tg_ws) return;
+    L->tg_ws = static_cast<float*>(dmalloc(size_t(kTgMaxUnits) * 32 * 128 * 4, L->allocs));
+    L->tg_cnt = static_cast<int*>(dmalloc(size_t(kTgMaxTiles) * 4, L->allocs));
+    cuda_check(cudaMemset(L->tg_cnt, 0, size_t(kTgMaxTiles) * 4), "tgemv counters");
+}
+
+// Decode (swap) linear on tgemv (TMA ring + warp MMAs) instead of the tcgen05 swap-AB kernel?
+// Measured per path, model and partition size (profiles/r2_decode_linear_paths.txt): tgemv
+// wins at <= 16 tokens on weights >= 16 MB with K >= 2048 on Green Context partitions
+// (1.1-1.6x at 16-64 SMs for the 3B/8B projections) and, on the full device, where the weight
+// has enough 128-row tiles for one whole wave (no K split); the tcgen05 kernel keeps 17-32
+// tokens (tgemv is MMA-issue bound there: 256 m16n8k16 per 32 KiB stage) and the small 0.5B
+// projections.  ASB_NO_TGEMV=1: never (A/B baseline); ASB_TGEMV=1: every T <= 32 linear.
+bool use_tgemv(int T, const Weight& w, int num_sms) {
+    static const int mode = std::getenv("ASB_NO_TGEMV") && std::atoi(std::getenv("ASB_NO_TGEMV")) != 0 ? 0
+                            : std::getenv("ASB_TGEMV") && std::atoi(std::getenv("ASB_TGEMV")) != 0     ? 2
+                                                                                                        : 1;
+    if (mode == 0 || T > 32) return false;
+    if (mode == 2) return true;
+    const double bytes = 2.0 * double(w.rows) * w.cols;
+    const int tiles = w.rows_pad / 128;
+    return T <= 16 && bytes >= 16e6 && w.cols >= 2048 && (num_sms <= 120 || tiles * 5 >= num_sms * 4);
+}
+
+// Y[T][n_out] = X[T][k] . W^T with the path chosen by T (path 2 = dgemv, 3 = tgemv, 1 = tcgen05
 // swap-AB, 0 = tcgen05 normal).
 void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
             __nv_bfloat16* out, int ldo, const __nv_bfloat16* bias, const __nv_bfloat16* resid,
@@ -443,6 +475,41 @@ void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
         return;
     }
     if (xin.norm_w || xin.rows) fail(ASB_ERR_INVALID_ARGUMENT, "fused norm / row gather needs the dgemv path");
+    if (force_path == 3 || (force_path < 0 && use_tgemv(T, w, L->n_sms()))) {
+        if (T > 32) fail(ASB_ERR_INVALID_ARGUMENT, "tgemv takes <= 32 tokens");
+        tgemv_buffers(L);
+        TgemvParams d{};
+        d.T = T;
+        d.n_out = w.rows;
+        d.K = w.cols;
+        d.tiles = w.rows_pad / 128;
+        d.splits = force_splits;
+        d.epi = epi;
+        d.out = out;
+        d.out_f32 = out_f32;
+        d.ldo = ldo;
+        d.bias = bias;
+        d.resid = resid;
+        d.ldr = ldo;
+        if (rope) d.rope = *rope;
+        d.amax = amax;
+        if (post) d.post = *post;
+        d.ws = L->tg_ws;
+        d.cnt = L->tg_cnt;
+        static const bool tg_load_only = std::getenv("ASB_DEBUG_SKIP") &&
+                                         std::string(std::getenv("ASB_DEBUG_SKIP")).find("tgmath") != std::string::npos;
+        d.dbg_load_only = tg_load_only ? 1 : 0;
+        if (d.tiles > kTgMaxTiles || (force_splits > 1 && d.tiles * force_splits > kTgMaxUnits))
+            fail(ASB_ERR_INVALID_ARGUMENT, "tgemv: work units exceed the split workspace");
+        L->n_launch += 1;
+        const double units = 2.0 * (double(w.rows) * w.cols + double(T) * w.cols) +
+                             double(T) * w.rows * (epi == EPI_F32 ? 4.0 : 2.0);
+        cudaError_t e = cudaSuccess;
+        L->timed(ASB_STAT_DECODE_GEMM, units,
+                 [&] { e = tgemv_launch(w.map_a128k2, xmaps[T <= 16 ? 7 : 5], d, L->n_sms(), L->stream); });
+        cuda_check(e, "tgemv launch");
+        return;
+    }
     GemmParams p{};
     p.amax = amax;
     if (post) p.post = *post;
@@ -840,6 +907,7 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
             dmalloc(size_t(dec_rows) * s.hq * L->max_splits * 2 * 4, L->allocs));
         L->dcnt = static_cast<int*>(dmalloc(size_t(dec_rows) * s.hkv * 4, L->allocs));
         L->post_cnt = static_cast<int*>(dmalloc(64, L->allocs));
+        tgemv_buffers(L.get());
         cuda_check(cudaMemset(L->post_cnt, 0, 64), "counters");
         cuda_check(cudaMemset(L->dcnt, 0, size_t(dec_rows) * s.hkv * 4), "counters");
         {
@@ -1340,7 +1408,7 @@ asb_status asb_debug_gemm_bench(const void* x, const void* w, void* out, int tok
             cuda_check(pack_weights(static_cast<const __nv_bfloat16*>(w), W.ptr, n_out, k, nullptr), "pack");
             weight_maps(W);
         }
-        CUtensorMap xm[7];
+        CUtensorMap xm[8];
         act_maps(xm, x, tokens, k);
         asb_model fake;
         int dev = 0;
@@ -1395,7 +1463,7 @@ asb_status asb_debug_gemm(const void* x, const void* w, const void* bias, const 
         cuda_check(pack_weights(static_cast<const __nv_bfloat16*>(w), W.ptr, n_out, k,
                                 static_cast<cudaStream_t>(stream)), "pack");
         weight_maps(W);
-        CUtensorMap xm[7];
+        CUtensorMap xm[8];
         act_maps(xm, x, tokens, k);
         asb_lane tmp;  // only stream and sms are used by linear()
         asb_model fake;

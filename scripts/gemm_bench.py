@@ -1,4 +1,4 @@
-"""Decode linear-layer micro-bench: tcgen05 swap-AB (path 1) vs small-batch dgemv (path 2).
+"""Decode linear-layer micro-bench: tcgen05 swap-AB (path 1) vs small-batch dgemv (path 2) vs the TMA-ring warp-MMA tgemv (path 3).
 
 Back-to-back launches with PDL (asb_debug_gemm_bench), weights packed once; reports us per
 launch and algorithmic GB/s (weights + X + Y bytes) against the measured HBM peak.
@@ -32,6 +32,9 @@ ap.add_argument("--levels", type=int, nargs="+", default=[0],
                 help="green-context decode levels (SMs = level x 16 on B200); 0 = whole device")
 ap.add_argument("--models", nargs="+", default=list(SHAPES))
 ap.add_argument("--out", default=None)
+ap.add_argument("--linears", nargs="*", default=None, help="only these linears (e.g. gate_up)")
+ap.add_argument("--paths", type=int, nargs="*", default=None, help="only these paths (1 tcgen05, 2 dgemv, 3 tgemv)")
+ap.add_argument("--iters", type=int, default=50)
 ap.add_argument("--prefill", action="store_true", help="normal (prefill) path 0 at the given token counts; TF/s")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
@@ -39,6 +42,8 @@ slots = Slots(0, levels=9, granularity=16)
 res = []
 for model in a.models:
     for name, N, K, epi in SHAPES[model]:
+        if a.linears and name not in a.linears:
+            continue
         w = (torch.randn(N, K, device=dev) * 0.02).bfloat16()
         for T in a.tokens:
             x = torch.randn(T, K, device=dev).bfloat16()
@@ -51,11 +56,13 @@ for model in a.models:
                     stream, _ = slots.bind(lev)
                     sms = slots.sm_counts(lev)[0]
                 row = {"model": model, "linear": name, "T": T, "N": N, "K": K, "sms": sms or 148}
-                paths = (0,) if a.prefill else ((1, 2) if T <= 32 else (1,))
+                paths = (0,) if a.prefill else ((1, 2, 3) if T <= 32 else (1,))
                 for path in paths:
+                    if a.paths and path not in a.paths:
+                        continue
                     us = C.c_float(0)
                     check(lib().asb_debug_gemm_bench(x.data_ptr(), w.data_ptr(), out.data_ptr(), T, N, K, epi, path,
-                                                     50, sms, stream, C.byref(us)))
+                                                     a.iters, sms, stream, C.byref(us)))
                     row[f"p{path}_us"] = round(us.value, 2)
                     row[f"p{path}_gbs"] = round(bytes_ / (us.value * 1e-6) / 1e9, 1)
                     if a.prefill:
@@ -64,6 +71,8 @@ for model in a.models:
                     row["p1_frac"] = round(row["p1_gbs"] / PEAK, 3)
                 if "p2_gbs" in row:
                     row["p2_frac"] = round(row["p2_gbs"] / PEAK, 3)
+                if "p3_gbs" in row:
+                    row["p3_frac"] = round(row["p3_gbs"] / PEAK, 3)
                 res.append(row)
                 print(json.dumps(row), flush=True)
         del w

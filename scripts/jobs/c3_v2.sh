@@ -1,0 +1,8 @@
+# re-measure the C3 ProfileBundle on the page-granular decode attention, then C3 AgentServe vs FCFS
+python -m paper_2603_10342_b200.profile_measure --model llama3.2-3b --decode-batch 16 --decode-ctx 3000 --cold 3000 --resume 64 --resume-ctx 3000 --out gpurun_out/b200_profile_llama3.2-3b.json > /dev/null 2> gpurun_out/prof3b.log
+cp gpurun_out/b200_profile_llama3.2-3b.json profiles/
+python -c "
+import json; from paper_2603_10342_b200 import workloads as w
+p,m=w.load_profile('llama3.2-3b'); print(json.dumps(w.calibrate(p,m)))"
+for spec in agentserve mixed_fcfs; do echo "=== $spec"; timeout 300 python scripts/episode_timeline.py --config c3 --spec $spec; done
+timeout 1500 python scripts/policy_compare.py --config c3 --reps 3 --runs agentserve mixed_fcfs agentserve:rbase=2,r0=2 agentserve:slack=2.0 --out gpurun_out/pc_c3_v2.json 2>&1 | tail -8

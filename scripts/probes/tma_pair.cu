@@ -56,6 +56,46 @@ __global__ void __launch_bounds__(64, 1) stream_pair(const __grid_constant__ CUt
     }
 }
 
+// the same ring over the tile-packed weight layout: CTA c streams tiles c, c + grid, ... (all
+// k-units of a tile in order), as tgemv does with one split
+__global__ void __launch_bounds__(64, 1) stream_packed(const __grid_constant__ CUtensorMap pmap,
+                                                       const __grid_constant__ CUtensorMap xmap, int tiles, int kunits,
+                                                       int stages, unsigned long long* sink) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    const int stage_bytes = 32768 + 4096;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)stages * stage_bytes);
+    uint64_t* empty = full + stages;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint64_t pw = policy_evict_first(), px = policy_evict_last();
+        int i = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x)
+            for (int ku = 0; ku < kunits; ++ku, ++i) {
+                const int st = i % stages;
+                mbar_wait(&empty[st], ((i / stages) & 1) ^ 1);
+                mbar_expect_tx(&full[st], stage_bytes);
+                uint8_t* d = sm + (size_t)st * stage_bytes;
+                tma_load_4d_hint(d, &pmap, &full[st], 0, 0, 2 * ku, tile, pw);
+                tma_load_3d_hint(d + 32768, &xmap, &full[st], 0, 0, ku % 16, px);
+            }
+    } else if (threadIdx.x == 32) {
+        unsigned long long acc = 0;
+        int i = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x)
+            for (int ku = 0; ku < kunits; ++ku, ++i) {
+                const int st = i % stages;
+                mbar_wait(&full[st], (i / stages) & 1);
+                acc += sm[(size_t)st * stage_bytes + (i & 63)];
+                mbar_arrive(&empty[st]);
+            }
+        sink[blockIdx.x] = acc;
+    }
+}
+
 int main() {
     const size_t bytes = 1ull << 30;
     void *buf, *xbuf;
@@ -65,6 +105,30 @@ int main() {
     cudaMemset(xbuf, 1, 16 << 20);
     unsigned long long* sink;
     cudaMalloc(&sink, 1024 * 8);
+    {  // packed weight layout [tiles][kb][128][64] through the 4-D map the GEMMs use, box (64,128,2,1)
+        const int K = 3072, kbs = K / 64, tiles = (int)(bytes / (size_t(K) * 128 * 2));
+        CUtensorMap pmap, xmap;
+        make_tmap_packed(&pmap, buf, tiles * 128, K, 1, 2);
+        make_tmap_bf16_3d(&xmap, xbuf, 64, 32, 16, 32, 1);  // box 32 rows x 128 B = 4 KiB
+        for (int ctas : {16, 32, 64, 148})
+            for (int stages : {4, 5, 6}) {
+                const int wb = 32768, xb = 4096, smem = stages * (wb + xb) + 2 * stages * 8 + 1024;
+                cudaFuncSetAttribute(stream_packed, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                stream_packed<<<ctas, 64, smem>>>(pmap, xmap, tiles, kbs / 2, stages, sink);
+                cudaEvent_t e0, e1;
+                cudaEventCreate(&e0);
+                cudaEventCreate(&e1);
+                cudaEventRecord(e0);
+                stream_packed<<<ctas, 64, smem>>>(pmap, xmap, tiles, kbs / 2, stages, sink);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, e0, e1);
+                const double gbs = (double)tiles * K * 128 * 2 / (ms * 1e-3) / 1e9;
+                printf("packed 4-D w 32 KiB + x 4 KiB, CTAs %3d, stages %d: %7.1f GB/s  %6.1f GB/s/CTA  %s\n", ctas, stages,
+                       gbs, gbs / ctas, cudaGetErrorString(cudaGetLastError()));
+            }
+    }
     for (int w_kb : {32, 64}) {
         const int w_bytes = w_kb * 1024, w_rows = w_bytes / 128;
         CUtensorMap wmap;

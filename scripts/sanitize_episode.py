@@ -33,7 +33,7 @@ wall = {"workload": {"paradigm": "react", "concurrency": 4, "stagger_ms": 5.0, "
                      "resume": {"min": 300, "max": 300, "mean": 300},
                      "decode": {"min": 6, "max": 10, "mean": 8},
                      "tool_delay": {"kind": "fixed", "ms": 3.0}},
-        "slo": {"tau_tpot_ms": 5.0, "tau_ttft_ms": 500.0}, "seed": 13,
+        "slo": {"tau_tpot_ms": 20.0, "tau_ttft_ms": 2000.0}, "seed": 13,
         "controller": {"delta_t_ms": 20.0},
         "backend": {"clock": "wall", "model": "tiny", "prefill_unit_tokens": 128, "lend_idle_prefill": True}}
 for pol in (["agentserve"] if quick else ["agentserve", "mixed_fcfs", "static_partition"]):

@@ -1,5 +1,6 @@
 """Linear-layer kernels vs a plain torch fp32 reference (K5): the tcgen05 GEMM in both operand
-orders (normal / swap-AB, split-K) and the small-batch dgemv path, with every fused epilogue."""
+orders (normal / swap-AB, split-K), the small-batch dgemv path and the TMA-ring tgemv path,
+with every fused epilogue."""
 import pytest
 import torch
 
@@ -33,6 +34,11 @@ def _ref(x, w, bias, resid, epi):
     # path 2: small-batch dgemv (legacy warp MMA fed from HBM), T <= 32, ragged N
     (1, 4096, 256, 2, 0), (8, 1152, 896, 2, 0), (13, 896, 4864, 2, 0), (16, 9728, 896, 2, 0),
     (24, 512, 256, 2, 0), (32, 1000, 640, 2, 0), (5, 136, 3072, 2, 0),
+    # path 3: tgemv (TMA smem ring + warp MMA), T <= 32: chosen K splits, forced splits with the
+    # last-arriver reduction, ragged N, an odd k-block count (half-OOB last k-unit)
+    (1, 4096, 256, 3, 0), (8, 1152, 896, 3, 0), (13, 896, 4864, 3, 0), (16, 9728, 896, 3, 0),
+    (24, 512, 256, 3, 0), (32, 1000, 640, 3, 0), (5, 136, 3072, 3, 0), (17, 3072, 3072, 3, 4),
+    (31, 1000, 704, 3, 3), (9, 256, 8192, 3, 8),
 ])
 @pytest.mark.parametrize("epi", [EPI_BF16, EPI_RESID, EPI_SILU, EPI_F32])
 def test_gemm(T, N, K, path, splits, epi):
