@@ -79,5 +79,6 @@ cudaError_t decode_attention(const CUtensorMap& tmap_kv, const __nv_bfloat16* q,
                              const AttnShape& s, cudaStream_t stream);
 
 int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits);
+int decode_splits_persist(int base, int pages, int num_sms, int max_splits);
 
 }  // namespace asb

@@ -69,6 +69,71 @@ __device__ __forceinline__ uint32_t kv_off(int kv, int r, int c) {
     return line * 128 + (((c & 7) ^ (r & 7)) << 4);
 }
 
+// One 64-token K|V block of the online softmax for this warp's 16 keys (kw..kw+15 of the
+// block, absolute key index kbase + ..): S^T = K Q^T, running max / sum per head column,
+// O^T = alpha O^T + V^T P^T.
+template <int HD>
+__device__ __forceinline__ void attn_page(uint32_t base, int kw, int kbase, int ctx_len, const uint32_t (&qb)[HD / 16][2],
+                                          float (&o)[HD / 16][4], float (&m_run)[2], float (&l_run)[2],
+                                          float scale_log2, int lane) {
+    constexpr int MT = HD / 16;
+    const int g = lane >> 2, mi = lane >> 3;
+    // ---- S^T = K . Q^T : 16 keys x 8 heads, two accumulation chains over the dims
+    float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+        const int key = kw + (mi & 1) * 8 + (lane & 7);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4(base + kv_off<HD>(0, key, 2 * kk + (mi >> 1)), a0, a1, a2, a3);
+            if (kk & 1) mma16816(sb, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+            else mma16816(sa, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+        }
+    }
+    // ---- online softmax per head column: values (key g | g+8, head 2t + j)
+    const bool ok0 = kbase + g < ctx_len, ok1 = kbase + g + 8 < ctx_len;
+    float sv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const bool ok = e < 2 ? ok0 : ok1;
+        sv[e] = ok ? (sa[e] + sb[e]) * scale_log2 : -FLT_MAX;
+    }
+    float alpha[2], mx[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        float m = fmaxf(m_run[j], fmaxf(sv[j], sv[2 + j]));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+        mx[j] = m;
+        alpha[j] = exp2f(m_run[j] - m);
+        m_run[j] = m;
+    }
+    float p[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p[e] = sv[e] == -FLT_MAX ? 0.f : exp2f(sv[e] - mx[e & 1]);
+    const uint32_t p01 = pack_bf16(p[0], p[1]), p23 = pack_bf16(p[2], p[3]);
+    // sum what P.V will actually use (the bf16-rounded weights)
+    l_run[0] = l_run[0] * alpha[0] + (bf16_lo(p01) + bf16_lo(p23));
+    l_run[1] = l_run[1] * alpha[1] + (bf16_hi(p01) + bf16_hi(p23));
+    // P^T B-fragments: (keys 2t, 2t+1 | 2t+8, 2t+9; head g)
+    const uint32_t b0 = movmatrix_t(p01), b1 = movmatrix_t(p23);
+    // ---- O^T = alpha O^T + V^T . P^T : MT m-tiles of 16 dims
+    {
+        const int key = kw + (mi >> 1) * 8 + (lane & 7);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4_t(base + kv_off<HD>(1, key, 2 * mt + (mi & 1)), a0, a1, a2, a3);
+            o[mt][0] *= alpha[0];
+            o[mt][1] *= alpha[1];
+            o[mt][2] *= alpha[0];
+            o[mt][3] *= alpha[1];
+            mma16816(o[mt], a0, a1, a2, a3, b0, b1);
+        }
+    }
+}
+
 template <int HD>
 __global__ void __launch_bounds__(kThreadsD, 2)
     decode_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv,
@@ -181,62 +246,8 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             if (lane == 0) mbar_arrive(&empty[st]);
             continue;
         }
-        const uint32_t base = smem_u32(ring + st * C::kStage);
-        // ---- S^T = K . Q^T : 16 keys x 8 heads, two accumulation chains over the dims
-        float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
-        {
-            const int key = kw + (mi & 1) * 8 + (lane & 7);
-#pragma unroll
-            for (int kk = 0; kk < HD / 16; ++kk) {
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4(base + kv_off<HD>(0, key, 2 * kk + (mi >> 1)), a0, a1, a2, a3);
-                if (kk & 1) mma16816(sb, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
-                else mma16816(sa, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
-            }
-        }
-        // ---- online softmax per head column: values (key g | g+8, head 2t + j)
-        const int kbase = (p0 + i) * kBlockTokens + kw;
-        const bool ok0 = kbase + g < it.ctx_len, ok1 = kbase + g + 8 < it.ctx_len;
-        float sv[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const bool ok = e < 2 ? ok0 : ok1;
-            sv[e] = ok ? (sa[e] + sb[e]) * s.scale_log2 : -FLT_MAX;
-        }
-        float alpha[2], mx[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            float m = fmaxf(m_run[j], fmaxf(sv[j], sv[2 + j]));
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
-            mx[j] = m;
-            alpha[j] = exp2f(m_run[j] - m);
-            m_run[j] = m;
-        }
-        float p[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) p[e] = sv[e] == -FLT_MAX ? 0.f : exp2f(sv[e] - mx[e & 1]);
-        const uint32_t p01 = pack_bf16(p[0], p[1]), p23 = pack_bf16(p[2], p[3]);
-        // sum what P.V will actually use (the bf16-rounded weights)
-        l_run[0] = l_run[0] * alpha[0] + (bf16_lo(p01) + bf16_lo(p23));
-        l_run[1] = l_run[1] * alpha[1] + (bf16_hi(p01) + bf16_hi(p23));
-        // P^T B-fragments: (keys 2t, 2t+1 | 2t+8, 2t+9; head g)
-        const uint32_t b0 = movmatrix_t(p01), b1 = movmatrix_t(p23);
-        // ---- O^T = alpha O^T + V^T . P^T : MT m-tiles of 16 dims
-        {
-            const int key = kw + (mi >> 1) * 8 + (lane & 7);
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4_t(base + kv_off<HD>(1, key, 2 * mt + (mi & 1)), a0, a1, a2, a3);
-                o[mt][0] *= alpha[0];
-                o[mt][1] *= alpha[1];
-                o[mt][2] *= alpha[0];
-                o[mt][3] *= alpha[1];
-                mma16816(o[mt], a0, a1, a2, a3, b0, b1);
-            }
-        }
+        attn_page<HD>(smem_u32(ring + st * C::kStage), kw, (p0 + i) * kBlockTokens + kw, it.ctx_len, qb, o, m_run,
+                      l_run, s.scale_log2, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
     }
@@ -434,6 +445,248 @@ __global__ void decode_combine_kernel(const DecodeItem* __restrict__ items,
     out[(size_t)items[row].q_row * hq * HD + h * HD + d] = __float2bfloat16_rn(O / L);
 }
 
+// Persistent form for grids of more than one wave (small Green Context partitions): one wave
+// of CTAs (two per SM) walks the (row, kv head, split) units round-robin, the producer streams
+// the next unit's blocks while the consumers finish the current one (no CTA prologue / ring
+// fill per unit).  The block a unit ends on is held past its last use as the warps' merge
+// scratch and released after the unit's output; splits merge through fp32 partials by the
+// last-arriving split (the arithmetic of the non-persistent path, split order: deterministic).
+template <int HD>
+__global__ void __launch_bounds__(kThreadsD, 2)
+    decode_attn_persist_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_bfloat16* __restrict__ q,
+                               const DecodeItem* __restrict__ items, const int32_t* __restrict__ tables,
+                               __nv_bfloat16* __restrict__ out, float* __restrict__ part_o,
+                               float* __restrict__ part_ml, int* __restrict__ counters, int n_items, int splits,
+                               int pps, AttnShape s) {
+    using C = DC<HD>;
+    constexpr int MT = HD / 16;
+    constexpr int kS = C::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+    uint8_t* ring = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kRing);
+    uint64_t* empty = full + kS;
+    float* mls = reinterpret_cast<float*>(empty + kS);  // [warp][8][2]
+    float* wsp = mls + kWarps * 16;                      // [8][16] split m -> weights (last arriver)
+    float* lsp = wsp + 8 * 16;                           // [8][16] split l
+    float* linv = lsp + 8 * 16;                          // [8]
+    __shared__ int s_last;
+
+    const int G = s.hq / s.hkv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int units = n_items * s.hkv * splits;
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&tmap_kv);
+        for (int i = 0; i < kS; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    pdl_trigger();
+
+    if (warp == kWarps) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            bool waited = false;
+            int gi = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                const int item = u / (s.hkv * splits), kvh = (u / splits) % s.hkv, sp = u % splits;
+                const DecodeItem it = items[item];
+                const int n_pages = (it.ctx_len + kBlockTokens - 1) / kBlockTokens;
+                const int p0 = sp * pps, n_local = max(0, min(n_pages, p0 + pps) - p0);
+                const int new_page = (it.ctx_len - 1) / kBlockTokens;
+                const int32_t* table = tables + it.table_off;
+                for (int i = 0; i < n_local; ++i, ++gi) {
+                    // only the block holding this step's token depends on the kernel before us
+                    if (!waited && p0 + i >= new_page) {
+                        pdl_wait();
+                        waited = true;
+                    }
+                    const int st = gi % kS;
+                    mbar_wait(&empty[st], ((gi / kS) & 1) ^ 1);
+                    mbar_expect_tx(&full[st], C::kStage);
+                    const int page = (s.layer * s.num_blocks + table[p0 + i]) * s.hkv + kvh;
+                    tma_load_5d_hint(ring + st * C::kStage, &tmap_kv, &full[st], 0, 0, 0, 0, page, pol);
+                }
+            }
+            if (!waited) pdl_wait();
+        }
+        return;  // the producer warp takes no part in the consumers' named barriers
+    }
+
+    // ---------------------------------------------------------------- consumers
+    pdl_wait();  // q comes from the kernel before us
+    const int tid = threadIdx.x;
+    const int g = lane >> 2, t = lane & 3;
+    const int kw = warp * 16;
+    int gi = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int item = u / (s.hkv * splits), kvh = (u / splits) % s.hkv, sp = u % splits;
+        const DecodeItem it = items[item];
+        const int n_pages = (it.ctx_len + kBlockTokens - 1) / kBlockTokens;
+        const int p0 = sp * pps, n_local = max(0, min(n_pages, p0 + pps) - p0);
+        uint32_t qb[HD / 16][2];
+        {
+            const __nv_bfloat16* qrow = q + (size_t)it.q_row * s.hq * HD + (size_t)(kvh * G + g) * HD;
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk) {
+                if (g < G) {
+                    qb[kk][0] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t);
+                    qb[kk][1] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t + 8);
+                } else {
+                    qb[kk][0] = qb[kk][1] = 0u;
+                }
+            }
+        }
+        float o[MT][4];
+#pragma unroll
+        for (int n = 0; n < MT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+        float m_run[2] = {-FLT_MAX, -FLT_MAX}, l_run[2] = {0.f, 0.f};
+        int st = 0;
+        for (int i = 0; i < n_local; ++i, ++gi) {
+            st = gi % kS;
+            mbar_wait(&full[st], (gi / kS) & 1);
+            if (!s.dbg_load_only)
+                attn_page<HD>(smem_u32(ring + st * C::kStage), kw, (p0 + i) * kBlockTokens + kw, it.ctx_len, qb, o,
+                              m_run, l_run, s.scale_log2, lane);
+            __syncwarp();
+            if (lane == 0 && i + 1 < n_local) mbar_arrive(&empty[st]);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            l_run[j] += __shfl_xor_sync(0xffffffffu, l_run[j], 4);
+            l_run[j] += __shfl_xor_sync(0xffffffffu, l_run[j], 8);
+            l_run[j] += __shfl_xor_sync(0xffffffffu, l_run[j], 16);
+        }
+        const size_t slot0 = ((size_t)item * s.hq + kvh * G) * splits + sp;  // head h: slot0 + h * splits
+        if (n_local > 0) {
+            // ---- merge the warps through the held block, then this unit's output
+            float* mrg = reinterpret_cast<float*>(ring + st * C::kStage);  // [warp][8][HD]
+            named_sync(1, kWarps * 32);
+            float* mw = mrg + warp * 8 * HD;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int h = 2 * t + j;
+                if (h < G) {
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        mw[h * HD + mt * 16 + g] = o[mt][j];
+                        mw[h * HD + mt * 16 + g + 8] = o[mt][2 + j];
+                    }
+                    if (g == 0) {
+                        mls[(warp * 8 + h) * 2] = m_run[j];
+                        mls[(warp * 8 + h) * 2 + 1] = l_run[j];
+                    }
+                }
+            }
+            named_sync(1, kWarps * 32);
+            for (int e = tid; e < G * HD; e += kWarps * 32) {
+                const int h = e / HD, d = e % HD;
+                float M = -FLT_MAX;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) M = fmaxf(M, mls[(w * 8 + h) * 2]);
+                float L = 0.f, O = 0.f;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) {
+                    const float lw = mls[(w * 8 + h) * 2 + 1];
+                    if (lw == 0.f) continue;
+                    const float f = exp2f(mls[(w * 8 + h) * 2] - M);
+                    L += lw * f;
+                    O += mrg[(w * 8 + h) * HD + d] * f;
+                }
+                if (splits == 1) {
+                    out[(size_t)it.q_row * s.hq * HD + (kvh * G + h) * HD + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+                } else {
+                    const size_t sl = slot0 + (size_t)h * splits;
+                    part_o[sl * HD + d] = O;
+                    if (d == 0) {
+                        part_ml[sl * 2 + 0] = M;
+                        part_ml[sl * 2 + 1] = L;
+                    }
+                }
+            }
+            named_sync(1, kWarps * 32);  // done with the held block
+            if (lane == 0) mbar_arrive(&empty[st]);
+        } else if (tid < G) {
+            // an empty split (ragged contexts): contributes nothing to the merge
+            const size_t sl = slot0 + (size_t)tid * splits;
+            part_ml[sl * 2 + 0] = -FLT_MAX;
+            part_ml[sl * 2 + 1] = 0.f;
+        }
+        if (splits == 1) continue;
+        // ---- last-arriving split of (row, kv head) merges all splits in split order
+        __threadfence();
+        named_sync(1, kWarps * 32);
+        if (tid == 0) {
+            int* cnt = counters + item * s.hkv + kvh;
+            const int prev = atomicAdd(cnt, 1);
+            s_last = prev == splits - 1;
+            if (s_last) *cnt = 0;
+        }
+        named_sync(1, kWarps * 32);
+        if (!s_last) continue;
+        __threadfence();
+        for (int i = tid; i < G * splits; i += kWarps * 32) {
+            const int h = i / splits, q2 = i % splits;
+            const size_t sl = ((size_t)item * s.hq + kvh * G + h) * splits + q2;
+            wsp[h * 16 + q2] = __ldcg(part_ml + sl * 2);
+            lsp[h * 16 + q2] = __ldcg(part_ml + sl * 2 + 1);
+        }
+        named_sync(1, kWarps * 32);
+        if (tid < G) {
+            float M = -FLT_MAX;
+            for (int q2 = 0; q2 < splits; ++q2) M = fmaxf(M, wsp[tid * 16 + q2]);
+            float L = 0.f;
+            for (int q2 = 0; q2 < splits; ++q2) {
+                const float ls = lsp[tid * 16 + q2];
+                const float w = ls == 0.f ? 0.f : exp2f(wsp[tid * 16 + q2] - M);
+                wsp[tid * 16 + q2] = w;
+                L += ls * w;
+            }
+            linv[tid] = L;
+        }
+        named_sync(1, kWarps * 32);
+        for (int e = tid; e < G * HD; e += kWarps * 32) {
+            const int h = e / HD, d = e % HD;
+            const float* po = part_o + (((size_t)item * s.hq + kvh * G + h) * splits) * HD + d;
+            float pv[16];
+#pragma unroll
+            for (int q2 = 0; q2 < 16; ++q2) pv[q2] = q2 < splits ? __ldcg(po + (size_t)q2 * HD) : 0.f;
+            float O = 0.f;
+#pragma unroll
+            for (int q2 = 0; q2 < 16; ++q2) {
+                const float w = q2 < splits ? wsp[h * 16 + q2] : 0.f;
+                if (w != 0.f) O += pv[q2] * w;
+            }
+            out[(size_t)it.q_row * s.hq * HD + (kvh * G + h) * HD + d] = __float2bfloat16_rn(O / linv[h]);
+        }
+        named_sync(1, kWarps * 32);  // wsp / mls reused by the next unit
+    }
+}
+
+template <int HD>
+cudaError_t launch_persist(const CUtensorMap& tkv, const __nv_bfloat16* q, const DecodeItem* items, int n_items,
+                           int splits, int pps, const int32_t* tables, __nv_bfloat16* out, float* po, float* pml,
+                           int* cnt, int num_sms, const AttnShape& s, cudaStream_t st) {
+    using C = DC<HD>;
+    const int smem = C::kRing + 2 * C::kStages * 8 + (kWarps * 16 + 2 * 8 * 16 + 8) * 4 + 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e =
+            cudaFuncSetAttribute(decode_attn_persist_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int units = n_items * s.hkv * splits;
+    const int grid = std::min(units, 2 * std::max(1, num_sms));
+    return launch_k(decode_attn_persist_kernel<HD>, dim3(grid), dim3(kThreadsD), smem, st, tkv, q, items, tables, out,
+                    po, pml, cnt, n_items, splits, pps, s);
+}
+
 template <int HD>
 cudaError_t launch_hd(const CUtensorMap& tkv, const __nv_bfloat16* q, const DecodeItem* items, int n_items,
                       int splits, int pps, const int32_t* tables, __nv_bfloat16* out, float* po, float* pml,
@@ -508,6 +761,23 @@ int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits
     return best;
 }
 
+int decode_splits_persist(int base, int pages, int num_sms, int max_splits) {
+    // persistent one-wave grid: makespan = units per CTA x (blocks per unit + per-unit
+    // overhead: q load + warp merge ~1 block, +1 for the split merge)
+    const int slots = 2 * std::max(num_sms, 1);
+    int best = 1;
+    long best_t = -1;
+    for (int sp = 1; sp <= std::min(max_splits, 16); ++sp) {
+        if (sp > 1 && (pages + sp - 1) / sp < 3) break;
+        const long t = (long(base) * sp + slots - 1) / slots * ((pages + sp - 1) / sp + (sp > 1 ? 2 : 1));
+        if (best_t < 0 || t < best_t) {
+            best_t = t;
+            best = sp;
+        }
+    }
+    return best;
+}
+
 cudaError_t decode_attention(const CUtensorMap& tmap_kv, const __nv_bfloat16* q, const DecodeItem* items,
                              int n_items, int max_ctx, const int32_t* tables, __nv_bfloat16* out,
                              float* part_o, float* part_ml, int* counters, int max_splits, int num_sms,
@@ -521,6 +791,23 @@ cudaError_t decode_attention(const CUtensorMap& tmap_kv, const __nv_bfloat16* q,
                                   : decode_splits(n_items, s.hkv, max_ctx, num_sms,
                                                   no_cluster ? max_splits : std::min(max_splits, 8));
     const int pages = (max_ctx + kBlockTokens - 1) / kBlockTokens;
+    // more (row, kv head) items than one wave of CTAs (small partitions, large batches): the
+    // persistent kernel, splits by makespan with a per-unit overhead (ASB_DECODE_PERSIST=0: off)
+    static const int persist_env = std::getenv("ASB_DECODE_PERSIST") ? std::atoi(std::getenv("ASB_DECODE_PERSIST")) : -1;
+    const bool persist = force <= 0 && persist_env != 0 &&
+                         (persist_env == 1 || n_items * s.hkv > 2 * std::max(1, num_sms)) && counters;
+    if (persist) {
+        const int sp = decode_splits_persist(n_items * s.hkv, pages, num_sms, max_splits);
+        const int pps = (pages + sp - 1) / sp;
+        const int splits = (pages + pps - 1) / pps;
+        if (s.hd == 128)
+            return launch_persist<128>(tmap_kv, q, items, n_items, splits, pps, tables, out, part_o, part_ml, counters,
+                                       num_sms, s, stream);
+        if (s.hd == 64)
+            return launch_persist<64>(tmap_kv, q, items, n_items, splits, pps, tables, out, part_o, part_ml, counters,
+                                      num_sms, s, stream);
+        return cudaErrorInvalidValue;
+    }
     const int pps = (pages + splits0 - 1) / splits0;
     const int splits = (pages + pps - 1) / pps;
     if (s.hd == 128)

@@ -1,0 +1,8 @@
+# C3 ProfileBundle on the current kernels, then AgentServe variants vs FCFS (3 reps each)
+python -m paper_2603_10342_b200.profile_measure --model llama3.2-3b --decode-batch 16 --decode-ctx 3000 --cold 3000 --resume 64 --resume-ctx 3000 --out gpurun_out/b200_profile_llama3.2-3b.json > /dev/null 2> gpurun_out/prof3b.log
+cp gpurun_out/b200_profile_llama3.2-3b.json profiles/
+python -c "
+import json; from paper_2603_10342_b200 import workloads as w
+p,m=w.load_profile('llama3.2-3b'); print(json.dumps(w.calibrate(p,m)))"
+timeout 300 python scripts/episode_timeline.py --config c3 --spec agentserve
+timeout 2000 python scripts/policy_compare.py --config c3 --reps 3 --runs mixed_fcfs agentserve agentserve:slack=1.75 agentserve:slack=2.0 agentserve:rbase=2,r0=2 agentserve:tlow=0.7 --out gpurun_out/pc_c3_v3.json 2>&1 | tail -8

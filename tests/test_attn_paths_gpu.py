@@ -9,6 +9,8 @@ per process:
   no cluster, 16 splits -> fp32 partials merged by the grid's last-arriving CTA per row
   combine kernel        -> fp32 partials merged by decode_combine_kernel
   1 split               -> no merge at all on long contexts
+  persistent            -> one-wave persistent grid walking (row, kv head, split) units, held-block
+                           warp merge, last-arriver split merge incl. empty splits of ragged rows
 and both prefill-attention decompositions: the default work-unit list (only long causal items
 split, one wave) and the uniform grid.z split (ASB_PREFILL_UNITS=0, optionally forced to 3).
 """
@@ -32,7 +34,10 @@ CASE = "tests/test_forward_gpu.py::test_forward_matches_oracle[hd128-prompt_lens
     {"ASB_DECODE_MAX_SPLITS": "1"},
     {"ASB_PREFILL_UNITS": "0"},
     {"ASB_PREFILL_UNITS": "0", "ASB_PREFILL_SPLITS": "3"},
-], ids=["cluster3", "last_arriver16", "combine", "single", "prefill_uniform", "prefill_uniform3"])
+    {"ASB_DECODE_PERSIST": "1"},
+    {"ASB_DECODE_PERSIST": "1", "ASB_DECODE_MAX_SPLITS": "1"},
+], ids=["cluster3", "last_arriver16", "combine", "single", "prefill_uniform", "prefill_uniform3", "persistent",
+        "persistent_single"])
 def test_decode_attention_merge_paths(env):
     e = dict(os.environ)
     e.update(env)

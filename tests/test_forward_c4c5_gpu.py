@@ -167,7 +167,8 @@ def test_full_width_truncated_matches_oracle(case):
     {"ASB_DECODE_MAX_SPLITS": "1"},
     {"ASB_PREFILL_UNITS": "0"},
     {"ASB_PREFILL_UNITS": "0", "ASB_PREFILL_SPLITS": "3"},
-], ids=["cluster3", "last_arriver16", "combine", "single", "prefill_uniform", "prefill_uniform3"])
+    {"ASB_DECODE_PERSIST": "1"},
+], ids=["cluster3", "last_arriver16", "combine", "single", "prefill_uniform", "prefill_uniform3", "persistent"])
 def test_c4_layout_merge_paths(env):
     e = dict(os.environ)
     e.update(env)
