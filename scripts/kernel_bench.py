@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--decode", nargs="*", default=None, help="override decode cases, e.g. 16x3000 48x3000")
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--prefill", type=int, nargs="*", default=None, help="override prefill lengths")
     ap.add_argument("--level", type=int, default=0,
                     help="run the decode cases on the decode partition of this Green Context slot level")
     a = ap.parse_args()
@@ -47,8 +49,12 @@ def main():
         pls, dcs = CASES[name]
         if a.decode:
             dcs = [tuple(int(v) for v in c.split("x")) for c in a.decode]
+        if a.prefill:
+            pls = list(a.prefill)
         if a.no_prefill:
             pls = []
+        if a.no_decode:
+            dcs = []
         max_ctx = max([p for p in pls] + [c for _, c in dcs]) + 256
         pmax = max(pls + [256])
         m = Model(name, seed=13, max_context=max_ctx)
