@@ -30,15 +30,17 @@ namespace {
 // Two GQA-packed query tiles per CTA (256 MMA rows = 2 x (128/G tokens) x G heads of one KV
 // head) share every K/V page.  Roles:
 //   warp 0     TMA producer (Q once, K/V pages into a ring)
-//   warp 1     MMA issuer: S_t = Q_t.K^T into TMEM, then O_t += P_t.V with P_t read straight
-//              from TMEM (the A-from-TMEM form of tcgen05.mma); S of page j+1 for both tiles is
-//              issued before P.V of page j, so the tensor core runs while softmax works.
+//   warps 1,10 MMA issuers, one per tile: S_t = Q_t.K^T into TMEM, then O_t += P_t.V with P_t
+//              read straight from TMEM (the A-from-TMEM form of tcgen05.mma); S_t of page j+1
+//              is issued before P_t.V of page j, so the tensor core runs while softmax works.
+//              One issuer per tile decouples the tiles: a single in-order issuer made tile 0's
+//              next S wait for tile 1's softmax (and vice versa) every page.
 //   warps 2-5  softmax of tile 0, warps 6-9 softmax of tile 1: one query row per thread (its
 //              TMEM lane), P written back over its own S columns as packed bf16.
 // O accumulates in TMEM across pages.  The running max is refreshed lazily: O and l are
 // rescaled (in TMEM, by the row's own thread) only when a row max grows by more than 2^8, so
 // most pages never touch O outside the MMA.
-constexpr int kPThreads = 320;
+constexpr int kPThreads = 352;
 constexpr float kRescaleLog2 = 8.0f;
 
 template <int HD>
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         mbar_init(q_full, 1);
         for (int i = 0; i < C::kStages; ++i) {
             mbar_init(&kv_full[i], 1);
-            mbar_init(&kv_empty[i], 1);
+            mbar_init(&kv_empty[i], 2);  // released by both tiles' P.V
         }
         for (int i = 0; i < 4; ++i) {
             mbar_init(&s_full[i], 1);
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             }
         }
         __syncwarp();
-    } else if (warp == 1) {
+    } else if (warp == 1 || warp == 10) {
         constexpr uint32_t idesc_s = make_idesc_bf16(128, kBlockTokens, false, false);
         constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
         mbar_wait(q_full, 0);
@@ -225,24 +227,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                  (j > 0 || k > 0) ? 1u : 0u);
                 }
                 umma_commit(&pv_done[2 * t + b]);
-                if (t == 1) umma_commit(&kv_empty[st]);
+                umma_commit(&kv_empty[st]);
             }
             __syncwarp();
         };
         auto wait_kv = [&](int j) {
             mbar_wait(&kv_full[j % C::kStages], (j / C::kStages) & 1);
         };
+        const int t = warp == 1 ? 0 : 1;
         wait_kv(0);
-        issue_s(0, 0);
-        issue_s(1, 0);
+        issue_s(t, 0);
         for (int j = 0; j < n_kv; ++j) {
             if (j + 1 < n_kv) {
                 wait_kv(j + 1);
-                issue_s(0, j + 1);
-                issue_s(1, j + 1);
+                issue_s(t, j + 1);
             }
-            issue_pv(0, j);
-            issue_pv(1, j);
+            issue_pv(t, j);
         }
     } else {
         // softmax: tile t, one query row per thread (TMEM lane quarter = warp % 4)

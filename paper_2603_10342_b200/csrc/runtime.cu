@@ -566,9 +566,19 @@ void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
         p.b_packed = 1;
         p.M = T;
         p.N = w.rows;
+        // BN by wave quantisation: the tile count that fills whole waves of the persistent
+        // grid best.  A 128x128 UMMA reads as many operand bytes from smem per flop as the SMEM
+        // pipe delivers, so BN = 128 only wins by a wide fill margin at d >= 2048 (3B/7B/8B:
+        // 1016-1081 TF/s with it vs 1174-1226 with BN = 256 at C3-C5, profiles/r2_prefill_bn.txt)
+        // and by a small one for the 0.5B shapes; ASB_PREFILL_BN forces
         const int tm = (T + 127) / 128;
-        const int t256 = tm * ((w.rows + 255) / 256);
-        const int bn = (t256 < (num_sms * 4) / 5) ? 128 : 256;
+        const int t256 = tm * ((w.rows + 255) / 256), t128 = tm * ((w.rows + 127) / 128);
+        auto fill = [&](int tiles) {
+            const int waves = (tiles + num_sms - 1) / num_sms;
+            return double(tiles) / (double(waves) * num_sms);
+        };
+        static const int bn_env = std::getenv("ASB_PREFILL_BN") ? std::atoi(std::getenv("ASB_PREFILL_BN")) : 0;
+        const int bn = bn_env == 128 || bn_env == 256 ? bn_env : (fill(t128) * (w.cols <= 1024 ? 0.96 : 0.75) > fill(t256) ? 128 : 256);
         p.splits = 1;
         // normal path: B = W.  bn==128 reuses the box-128 weight map.
         e = gemm_launch(xmaps[0], bn == 256 ? w.map_b256 : w.map_a128, p, bn, num_sms, L->stream, pdl);
