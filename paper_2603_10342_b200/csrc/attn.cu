@@ -265,12 +265,33 @@ __global__ void __launch_bounds__(kPThreads, 1)
             tmem_ld32(s_col + 32, sb2);
             tmem_ld_wait();
             const int kbase = (blk0 + j) * kBlockTokens;
+            // pages left of the causal diagonal for every row of the warp take the unmasked
+            // path (no per-element compare/select); the row max is a 3-input FMNMX tree
             const bool full_vis = kbase + kBlockTokens - 1 <= qpos;
-            float mx = -FLT_MAX;
+            const bool warp_full = __all_sync(0xffffffffu, full_vis);
+            if (!warp_full) {
 #pragma unroll
-            for (int c = 0; c < 64; ++c) {
-                const float x = __uint_as_float(c < 32 ? sa[c] : sb2[c - 32]);
-                if (full_vis || kbase + c <= qpos) mx = fmaxf(mx, x);
+                for (int c = 0; c < 32; ++c) {
+                    if (kbase + c > qpos) sa[c] = __float_as_uint(-FLT_MAX);
+                    if (kbase + 32 + c > qpos) sb2[c] = __float_as_uint(-FLT_MAX);
+                }
+            }
+            float mx;
+            {
+                float m3[22];
+#pragma unroll
+                for (int c = 0; c < 21; ++c) {
+                    const int a = 3 * c;
+                    m3[c] = fmax3f(__uint_as_float(a < 32 ? sa[a] : sb2[a - 32]),
+                                   __uint_as_float(a + 1 < 32 ? sa[a + 1] : sb2[a + 1 - 32]),
+                                   __uint_as_float(a + 2 < 32 ? sa[a + 2] : sb2[a + 2 - 32]));
+                }
+                m3[21] = __uint_as_float(sb2[31]);
+                float m1[8];
+#pragma unroll
+                for (int c = 0; c < 7; ++c) m1[c] = fmax3f(m3[3 * c], m3[3 * c + 1], m3[3 * c + 2]);
+                m1[7] = m3[21];
+                mx = fmax3f(fmax3f(m1[0], m1[1], m1[2]), fmax3f(m1[3], m1[4], m1[5]), fmaxf(m1[6], m1[7]));
             }
             mx = mx == -FLT_MAX ? -FLT_MAX : mx * s.scale_log2;
             const bool need = mx > m_ref + kRescaleLog2;
@@ -296,19 +317,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     m_ref = mx;
                 }
             }
-            const float nm = -m_ref;
+            // no visible key yet (m_ref still -FLT_MAX): the masked -FLT_MAX scores must map to 0
+            const float nm = m_ref == -FLT_MAX ? 0.f : -m_ref;
             float psum = 0.f;
             uint32_t pk[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
                 const float x0 = __uint_as_float(c < 16 ? sa[2 * c] : sb2[2 * c - 32]);
                 const float x1 = __uint_as_float(c < 16 ? sa[2 * c + 1] : sb2[2 * c + 1 - 32]);
-                float p0 = exp2f(fmaf(x0, s.scale_log2, nm));
-                float p1 = exp2f(fmaf(x1, s.scale_log2, nm));
-                if (!full_vis) {
-                    p0 = (kbase + 2 * c <= qpos) ? p0 : 0.f;
-                    p1 = (kbase + 2 * c + 1 <= qpos) ? p1 : 0.f;
-                }
+                // masked keys hold -FLT_MAX: the FMA gives -inf-like input, ex2 flushes it to 0
+                const float p0 = ex2_ftz(fmaf(x0, s.scale_log2, nm));
+                const float p1 = ex2_ftz(fmaf(x1, s.scale_log2, nm));
                 psum += p0 + p1;
                 pk[c] = pack_bf16(p0, p1);
             }

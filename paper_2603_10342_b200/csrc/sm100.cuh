@@ -285,6 +285,18 @@ __host__ __device__ __forceinline__ int argmax_key_index(unsigned long long k) {
 }
 
 // ---------------------------------------------------------------- misc
+// 3-input max (FMNMX3, sm_100) and the flush-to-zero MUFU.EX2 (no denormal-range fixup: the
+// exp2f lowering spends FSETP + 2 FMUL + FSEL around every MUFU.EX2 for it)
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ float bf16_lo(uint32_t v) {
     return __uint_as_float(v << 16);
 }
