@@ -319,19 +319,24 @@ __global__ void __launch_bounds__(kPThreads, 1)
             }
             // no visible key yet (m_ref still -FLT_MAX): the masked -FLT_MAX scores must map to 0
             const float nm = m_ref == -FLT_MAX ? 0.f : -m_ref;
-            float psum = 0.f;
+            // key pairs on the packed fp32x2 pipe (FFMA2 / FADD2); masked keys hold -FLT_MAX:
+            // the FMA gives a huge negative input and ex2 flushes it to 0
+            const unsigned long long sc2 = f2_pack(s.scale_log2, s.scale_log2), nm2 = f2_pack(nm, nm);
+            unsigned long long acc2 = f2_pack(0.f, 0.f);
             uint32_t pk[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
                 const float x0 = __uint_as_float(c < 16 ? sa[2 * c] : sb2[2 * c - 32]);
                 const float x1 = __uint_as_float(c < 16 ? sa[2 * c + 1] : sb2[2 * c + 1 - 32]);
-                // masked keys hold -FLT_MAX: the FMA gives -inf-like input, ex2 flushes it to 0
-                const float p0 = ex2_ftz(fmaf(x0, s.scale_log2, nm));
-                const float p1 = ex2_ftz(fmaf(x1, s.scale_log2, nm));
-                psum += p0 + p1;
+                float y0, y1;
+                f2_unpack(ffma2(f2_pack(x0, x1), sc2, nm2), y0, y1);
+                const float p0 = ex2_ftz(y0), p1 = ex2_ftz(y1);
+                acc2 = fadd2(acc2, f2_pack(p0, p1));
                 pk[c] = pack_bf16(p0, p1);
             }
-            l_run += psum;
+            float ps0, ps1;
+            f2_unpack(acc2, ps0, ps1);
+            l_run += ps0 + ps1;
             tmem_st32(s_col, pk);  // P over its own S columns (A operand of P.V)
             tmem_st_wait();
             tc_fence_before();
