@@ -330,6 +330,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const float x1 = __uint_as_float(c < 16 ? sa[2 * c + 1] : sb2[2 * c + 1 - 32]);
                 float y0, y1;
                 f2_unpack(ffma2(f2_pack(x0, x1), sc2, nm2), y0, y1);
+                // (a quarter of the pairs through a degree-3 2^f on the FMA pipe instead of
+                // MUFU.EX2, FA4-style, measured slower: 943 -> 907 TF/s at C4 -- the softmax is
+                // bound by its per-warp dependency chain, not the XU pipe)
                 const float p0 = ex2_ftz(y0), p1 = ex2_ftz(y1);
                 acc2 = fadd2(acc2, f2_pack(p0, p1));
                 pk[c] = pack_bf16(p0, p1);
