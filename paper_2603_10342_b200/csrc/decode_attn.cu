@@ -101,23 +101,24 @@ __device__ __forceinline__ void attn_page(uint32_t base, int kw, int kbase, int 
     float alpha[2], mx[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-        float m = fmaxf(m_run[j], fmaxf(sv[j], sv[2 + j]));
+        float m = fmax3f(m_run[j], sv[j], sv[2 + j]);
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
         mx[j] = m;
-        alpha[j] = exp2f(m_run[j] - m);
+        alpha[j] = ex2_ftz(m_run[j] - m);
         m_run[j] = m;
     }
     float p[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) p[e] = sv[e] == -FLT_MAX ? 0.f : exp2f(sv[e] - mx[e & 1]);
+    for (int e = 0; e < 4; ++e) p[e] = sv[e] == -FLT_MAX ? 0.f : ex2_ftz(sv[e] - mx[e & 1]);
     const uint32_t p01 = pack_bf16(p[0], p[1]), p23 = pack_bf16(p[2], p[3]);
     // sum what P.V will actually use (the bf16-rounded weights)
     l_run[0] = l_run[0] * alpha[0] + (bf16_lo(p01) + bf16_lo(p23));
     l_run[1] = l_run[1] * alpha[1] + (bf16_hi(p01) + bf16_hi(p23));
     // P^T B-fragments: (keys 2t, 2t+1 | 2t+8, 2t+9; head g)
     const uint32_t b0 = movmatrix_t(p01), b1 = movmatrix_t(p23);
+    const unsigned long long al2 = f2_pack(alpha[0], alpha[1]);
     // ---- O^T = alpha O^T + V^T . P^T : MT m-tiles of 16 dims
     {
         const int key = kw + (mi >> 1) * 8 + (lane & 7);
@@ -125,10 +126,9 @@ __device__ __forceinline__ void attn_page(uint32_t base, int kw, int kbase, int 
         for (int mt = 0; mt < MT; ++mt) {
             uint32_t a0, a1, a2, a3;
             ldsm_x4_t(base + kv_off<HD>(1, key, 2 * mt + (mi & 1)), a0, a1, a2, a3);
-            o[mt][0] *= alpha[0];
-            o[mt][1] *= alpha[1];
-            o[mt][2] *= alpha[0];
-            o[mt][3] *= alpha[1];
+            // (dim g | g+8, heads 2t, 2t+1) pairs scale by (alpha0, alpha1) on the fp32x2 pipe
+            f2_unpack(fmul2(f2_pack(o[mt][0], o[mt][1]), al2), o[mt][0], o[mt][1]);
+            f2_unpack(fmul2(f2_pack(o[mt][2], o[mt][3]), al2), o[mt][2], o[mt][3]);
             mma16816(o[mt], a0, a1, a2, a3, b0, b1);
         }
     }
