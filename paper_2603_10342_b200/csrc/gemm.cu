@@ -438,8 +438,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tmem_ld32(t_row + c0 + H + sub, r2);
                         tmem_ld_wait();
                         if (ok) {
-                            const float* ct = R.cos_t + (size_t)pos * H + sub;
-                            const float* st = R.sin_t + (size_t)pos * H + sub;
+                            // each thread reads its own position's cos/sin row: 128-bit loads
+                            // (a warp-wide scalar load touches 32 rows = 32 L1 wavefronts; the
+                            // per-element form kept the LSU pipe 51% busy, profiles/
+                            // r2_ncu_prefill_qkv_epilogue.txt)
+                            const float4* ct = reinterpret_cast<const float4*>(R.cos_t + (size_t)pos * H + sub);
+                            const float4* st = reinterpret_cast<const float4*>(R.sin_t + (size_t)pos * H + sub);
+                            float cs[32], sn[32];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 c4 = ct[q], s4 = st[q];
+                                cs[4 * q] = c4.x, cs[4 * q + 1] = c4.y, cs[4 * q + 2] = c4.z, cs[4 * q + 3] = c4.w;
+                                sn[4 * q] = s4.x, sn[4 * q + 1] = s4.y, sn[4 * q + 2] = s4.z, sn[4 * q + 3] = s4.w;
+                            }
                             float y1[32], y2[32];
 #pragma unroll
                             for (int j = 0; j < 32; ++j) {
@@ -448,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     x1 += __bfloat162float(p.bias[f0 + sub + j]);
                                     x2 += __bfloat162float(p.bias[f0 + H + sub + j]);
                                 }
-                                rope2(bf16r(x1), bf16r(x2), ct[j], st[j], y1[j], y2[j]);
+                                rope2(bf16r(x1), bf16r(x2), cs[j], sn[j], y1[j], y2[j]);
                             }
                             store32_bf16(dst + sub, y1);
                             store32_bf16(dst + H + sub, y2);
