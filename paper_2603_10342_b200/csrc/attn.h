@@ -29,7 +29,8 @@ struct DecodeItem {
     int q_row;      // row in q / out
     int ctx_len;    // keys to attend (positions 0..ctx_len-1), includes the row's own token
     int table_off;  // block table offset
-    int pad;
+    int pad;        // first position of the row's session written by this forward (its blocks
+                    // are read only after the QKV kernel: PDL wait); ctx_len - 1 for a decode row
 };
 
 // KV pool page layout: [layer][block][kv_head][K rows 0..63 | V rows 0..63][hd] bf16 -- the K and

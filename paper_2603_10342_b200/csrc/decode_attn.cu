@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         // running, and wait for it only before the block that holds the new token.
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            const int new_page = (it.ctx_len - 1) / kBlockTokens;
+            const int new_page = it.pad / kBlockTokens;  // first block this step writes
             bool waited = false;
             for (int i = 0; i < n_local; ++i) {
                 if (!waited && p0 + i >= new_page) {
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                 const DecodeItem it = items[item];
                 const int n_pages = (it.ctx_len + kBlockTokens - 1) / kBlockTokens;
                 const int p0 = sp * pps, n_local = max(0, min(n_pages, p0 + pps) - p0);
-                const int new_page = (it.ctx_len - 1) / kBlockTokens;
+                const int new_page = it.pad / kBlockTokens;  // first block this step writes
                 const int32_t* table = tables + it.table_off;
                 for (int i = 0; i < n_local; ++i, ++gi) {
                     // only the block holding this step's token depends on the kernel before us

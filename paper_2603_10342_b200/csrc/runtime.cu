@@ -268,6 +268,7 @@ struct asb_lane {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int max_T = 0, max_segs = 0, max_tbl = 0, max_pitems = 0, max_splits = 16;
+    int max_ditems = 0;  // decode-attention rows: single-token rows + admitted-chunk tokens
     __nv_bfloat16 *x, *h, *qkv, *q, *attn, *act, *hl;
     float *logits, *part_o, *part_ml, *ppart_o, *ppart_ml;
     int* dcnt = nullptr;  // decode-attention split arrival counters [rows][hkv] (self-resetting)
@@ -910,7 +911,10 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->logits = static_cast<float*>(dmalloc(size_t(L->max_segs) * s.vocab * 4, L->allocs));
         if (std::getenv("ASB_GEMM_TIMELINE"))
             L->dbg_times = static_cast<unsigned long long*>(dmalloc(148 * 8 * 8, L->allocs));
-        const int dec_rows = std::min(L->max_segs, T);
+        // decode-attention rows: every single-token row plus the tokens of short segments (the
+        // admitted resume chunk of a decode step), each of which is its own causal decode row
+        L->max_ditems = std::min(T, L->max_segs + 32);
+        const int dec_rows = L->max_ditems;
         L->part_o = static_cast<float*>(
             dmalloc(size_t(dec_rows) * s.hq * L->max_splits * s.hd * 4, L->allocs));
         L->part_ml = static_cast<float*>(
@@ -930,7 +934,7 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->ppart_rows = size_t(4096) * 256 / 4;
         L->ppart_o = static_cast<float*>(dmalloc(L->ppart_rows * s.hd * 4, L->allocs));
         L->ppart_ml = static_cast<float*>(dmalloc(L->ppart_rows * 2 * 4, L->allocs));
-        L->meta_ints = size_t(3) * T + L->max_segs + L->max_tbl + 4 * size_t(L->max_segs) +
+        L->meta_ints = size_t(3) * T + L->max_segs + L->max_tbl + 4 * size_t(L->max_ditems) +
                        4 * size_t(L->max_pitems) + 64 +
                        4 * (size_t(L->max_pitems) + 512) + 4;  // prefill work units + combine list
         L->d_meta = static_cast<int32_t*>(dmalloc(L->meta_ints * 4, L->allocs));
@@ -1030,6 +1034,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         int n_logit = 0;
         std::vector<int32_t> tbl;
         std::vector<DecodeItem> ditems;
+        double dattn_seg_bytes = 0.0;  // algorithmic decode-attention bytes: each session's K/V once
         std::vector<PrefillItem> pitems;
         int max_ctx = 0, max_pblocks = 0;
         int row = 0;
@@ -1072,9 +1077,20 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                 h_pos[row + t] = p;
                 h_slot[row + t] = ss.blocks[p / kBlockTokens] * kBlockTokens + p % kBlockTokens;
             }
-            if (g.n_tokens == 1) {
-                ditems.push_back(DecodeItem{row, start + 1, toff, 0});
-                max_ctx = std::max(max_ctx, start + 1);
+            // A short segment (<= kChunkAsDecode tokens: the admitted resume chunk riding in a
+            // decode step) becomes one decode row per token, token t attending keys
+            // 0..start+t: exactly its causal prefix, read through the decode-attention kernel
+            // instead of a small, latency-bound prefill-attention launch (+ combine) per layer.
+            // DecodeItem.pad = the first position this forward writes for the row's session:
+            // blocks from there on are read only after the QKV kernel (PDL wait).
+            static const bool chunk_dec = !(std::getenv("ASB_CHUNK_AS_DECODE") &&
+                                            std::atoi(std::getenv("ASB_CHUNK_AS_DECODE")) == 0);
+            constexpr int kChunkAsDecode = 16;
+            if (g.n_tokens == 1 ||
+                (chunk_dec && g.n_tokens <= kChunkAsDecode && int(ditems.size()) + g.n_tokens <= L->max_ditems)) {
+                for (int t = 0; t < g.n_tokens; ++t) ditems.push_back(DecodeItem{row + t, start + t + 1, toff, start});
+                max_ctx = std::max(max_ctx, start + g.n_tokens);
+                dattn_seg_bytes += double(start + g.n_tokens) * s.hkv * s.hd * 2 * 2;  // K/V read once per session
             } else {
                 const int tpt = prefill_tokens_per_cta(s.hq, s.hkv);
                 for (int q0 = 0; q0 < g.n_tokens; q0 += tpt)
@@ -1090,7 +1106,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         std::memcpy(h_tbl, tbl.data(), tbl.size() * 4);
         int32_t* h_ditems = h_tbl + L->max_tbl;
         std::memcpy(h_ditems, ditems.data(), ditems.size() * sizeof(DecodeItem));
-        int32_t* h_pitems = h_ditems + 4 * L->max_segs;
+        int32_t* h_pitems = h_ditems + 4 * L->max_ditems;
         std::memcpy(h_pitems, pitems.data(), pitems.size() * sizeof(PrefillItem));
         // prefill work units (one wave, long causal items split; ASB_PREFILL_UNITS=0 off), int4-aligned
         static const bool units_off = std::getenv("ASB_PREFILL_UNITS") && std::atoi(std::getenv("ASB_PREFILL_UNITS")) == 0;
@@ -1114,7 +1130,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         const int32_t* d_tbl = d_lrows + L->max_segs;
         const DecodeItem* d_ditems = reinterpret_cast<const DecodeItem*>(d_tbl + L->max_tbl);
         const PrefillItem* d_pitems =
-            reinterpret_cast<const PrefillItem*>(d_tbl + L->max_tbl + 4 * L->max_segs);
+            reinterpret_cast<const PrefillItem*>(d_tbl + L->max_tbl + 4 * L->max_ditems);
         const int4* d_units = reinterpret_cast<const int4*>(L->d_meta + units_off_ints);
         const int4* d_comb = d_units + punits.size();
 
@@ -1143,7 +1159,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                                      : prefill_splits(int(pitems.size()), s.hkv, max_pblocks, L->n_sms(), L->ppart_rows);
         if (psplit_env > 0 && !pitems.empty())  // timing experiments: force the split count
             psplits = std::max(1, std::min({psplit_env, 32, int(L->ppart_rows / (pitems.size() * s.hkv * 256))}));
-        for (const auto& it : ditems) dattn_bytes += double(it.ctx_len) * s.hkv * s.hd * 2 * 2;
+        dattn_bytes = dattn_seg_bytes;
         for (const auto& it : pitems)
             pattn_flops += 4.0 * s.hd * s.hq *
                            (double(it.n_q) * it.q_pos0 + double(it.n_q) * (it.n_q + 1) / 2.0);

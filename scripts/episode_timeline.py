@@ -64,3 +64,29 @@ for s in sorted(arr, key=arr.get):
           f"{first.get(s, -1) - arr[s]:7.1f}")
 print("metrics", json.dumps({k: m.get(k) for k in ("ttft_p50_ms", "ttft_p95_ms", "ttft_p99_ms", "tpot_p50_ms",
                                                     "tpot_p95_ms", "tpot_p99_ms", "throughput_tps")}))
+# where the TPOT tail comes from: step duration by decode SM count and admitted-chunk presence
+import collections
+by = collections.defaultdict(list)
+for x in steps:
+    by[(x.get("sms", 0), int(x.get("chunk", 0)) > 0)].append(x["t"] - x["start"])
+print(f"{'sms':>4} {'chunk':>5} {'steps':>5} {'p50':>6} {'p95':>6} {'B_avg':>5}")
+for (sms, ch), v in sorted(by.items()):
+    v = sorted(v)
+    bs = [len(x["emit"]) for x in steps if x.get("sms", 0) == sms and (int(x.get("chunk", 0)) > 0) == ch]
+    print(f"{sms:4d} {str(ch):>5} {len(v):5d} {v[len(v) // 2]:6.2f} {v[int(0.95 * (len(v) - 1))]:6.2f} {sum(bs) / len(bs):5.1f}")
+gaps = []
+prev = {}
+for r in recs:
+    if r.get("k") == "issue" and r.get("req") == "decode":
+        prev[r["s"]] = None
+    elif r.get("k") == "step_done":
+        for s_ in r["emit"]:
+            if prev.get(s_) is not None:
+                gaps.append((r["t"] - prev[s_], r.get("sms", 0), int(r.get("chunk", 0)) > 0, r["t"]))
+            prev[s_] = r["t"]
+gaps.sort()
+p95 = gaps[int(0.95 * (len(gaps) - 1))][0]
+tail = [g for g in gaps if g[0] >= p95]
+print(f"TPOT gaps {len(gaps)}, p95 {p95:.2f} ms; gaps >= p95: by (sms, chunk):",
+      dict(collections.Counter((g[1], g[2]) for g in tail)),
+      "time range", round(min(g[3] for g in tail)), "-", round(max(g[3] for g in tail)))

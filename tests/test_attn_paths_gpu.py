@@ -11,7 +11,9 @@ per process:
   1 split               -> no merge at all on long contexts
   persistent            -> one-wave persistent grid walking (row, kv head, split) units, held-block
                            warp merge, last-arriver split merge incl. empty splits of ragged rows
-and both prefill-attention decompositions: the default work-unit list (only long causal items
+the admitted-resume chunk of a decode step through prefill attention (ASB_CHUNK_AS_DECODE=0)
+instead of one causal decode row per chunk token (the default), and both prefill-attention
+decompositions: the default work-unit list (only long causal items
 split, one wave) and the uniform grid.z split (ASB_PREFILL_UNITS=0, optionally forced to 3).
 """
 import os
@@ -36,8 +38,9 @@ CASE = "tests/test_forward_gpu.py::test_forward_matches_oracle[hd128-prompt_lens
     {"ASB_PREFILL_UNITS": "0", "ASB_PREFILL_SPLITS": "3"},
     {"ASB_DECODE_PERSIST": "1"},
     {"ASB_DECODE_PERSIST": "1", "ASB_DECODE_MAX_SPLITS": "1"},
+    {"ASB_CHUNK_AS_DECODE": "0"},
 ], ids=["cluster3", "last_arriver16", "combine", "single", "prefill_uniform", "prefill_uniform3", "persistent",
-        "persistent_single"])
+        "persistent_single", "chunk_as_prefill"])
 def test_decode_attention_merge_paths(env):
     e = dict(os.environ)
     e.update(env)
