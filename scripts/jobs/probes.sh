@@ -14,3 +14,5 @@ for L in 1 2 4 9; do
   echo "== attnmath level $L"; ASB_DEBUG_SKIP=attnmath run --models llama3.2-3b --decode 16x3000 32x3000 --level $L
   echo "== stages8 level $L"; ASB_DECODE_STAGES=8 run --models llama3.2-3b --decode 16x3000 32x3000 --level $L
 done
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2603_10342_b200/csrc scripts/probes/tma_pair.cu paper_2603_10342_b200/csrc/tmap.cpp -lcuda -o /tmp/tma_pair && /tmp/tma_pair
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2603_10342_b200/csrc scripts/probes/hmma.cu -o /tmp/hmma && /tmp/hmma
