@@ -38,8 +38,6 @@ namespace asb {
 
 namespace {
 
-constexpr int kTgWarps = 8;  // consumer warps: 2 row groups x 4 k groups
-constexpr int kTgThreads = (kTgWarps + 1) * 32;
 constexpr int kTgW = 128 * 128 * 2;  // 128 weight rows x 2 k-blocks
 constexpr int kTgRS = 33;            // red row stride (floats)
 
@@ -48,6 +46,13 @@ constexpr int kTgRS = 33;            // red row stride (floats)
 // scratch (red), so the other stages keep streaming the next unit meanwhile.
 template <int NT>
 struct TgCfg {
+    // consumer warps = RG row groups x 4 k groups: 8 warps (64 rows each) up to 16 tokens, 16
+    // warps (32 rows each) above, where the 4 n-tiles of MMAs per fragment need more warps in
+    // flight to keep the MMA pipe fed
+    static constexpr int kRG = NT <= 2 ? 2 : 4;
+    static constexpr int kWarps = 4 * kRG;
+    static constexpr int kThreads = (kWarps + 1) * 32;
+    static constexpr int kMT = 8 / kRG;  // 16-row m-tiles per warp
     static constexpr int kXRows = NT <= 2 ? 16 : 32;
     static constexpr int kX = kXRows * 128 * 2;
     static constexpr int kStage = kTgW + kX;
@@ -57,11 +62,12 @@ struct TgCfg {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(kTgThreads, 1)
+__global__ void __launch_bounds__(TgCfg<NT>::kThreads, 1)
     tgemv_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
                  const TgemvParams p) {
     using C = TgCfg<NT>;
     constexpr int kTgStages = C::kStages, kTgStage = C::kStage, kTgX = C::kX;
+    constexpr int kTgWarps = C::kWarps, MTW = C::kMT, RG = C::kRG;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
@@ -127,14 +133,14 @@ __global__ void __launch_bounds__(kTgThreads, 1)
         pdl_wait();  // residual / output buffers belong to the previous kernels
         const int tid = threadIdx.x;  // 0..255
         const int g = lane >> 2, t = lane & 3, mi = lane >> 3;
-        const int rg = warp & 1, kg = warp >> 1;
+        const int rg = warp % RG, kg = warp / RG;
         const int T = p.T;
         int i = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x) {
             const int tile = u / S, k0 = (u % S) * p.kups, k1 = min(p.kunits, k0 + p.kups);
-            float acc[4][NT][4];
+            float acc[MTW][NT][4];
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
+            for (int m = 0; m < MTW; ++m)
 #pragma unroll
                 for (int j = 0; j < NT; ++j) acc[m][j][0] = acc[m][j][1] = acc[m][j][2] = acc[m][j][3] = 0.f;
             for (int ku = k0; ku < k1; ++ku, ++i) {
@@ -153,8 +159,8 @@ __global__ void __launch_bounds__(kTgThreads, 1)
                                 b[jp][2], b[jp][3]);
                     }
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const int row = rg * 64 + m * 16 + (mi & 1) * 8 + (lane & 7), ch = cp + (mi >> 1);
+                    for (int m = 0; m < MTW; ++m) {
+                        const int row = rg * (128 / RG) + m * 16 + (mi & 1) * 8 + (lane & 7), ch = cp + (mi >> 1);
                         uint32_t a0, a1, a2, a3;
                         ldsm_x4(wst + (kb * 128 + row) * 128 + ((ch ^ (row & 7)) << 4), a0, a1, a2, a3);
 #pragma unroll
@@ -175,8 +181,8 @@ __global__ void __launch_bounds__(kTgThreads, 1)
             for (int r = 0; r < 4; ++r) {
                 if (kg == r) {
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const int rl = rg * 64 + m * 16 + g;
+                    for (int m = 0; m < MTW; ++m) {
+                        const int rl = rg * (128 / RG) + m * 16 + g;
 #pragma unroll
                         for (int j = 0; j < NT; ++j) {
                             const int tk = 8 * j + 2 * t;
@@ -322,7 +328,7 @@ cudaError_t launch_nt(const CUtensorMap& tw, const CUtensorMap& tx, const TgemvP
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    return launch_k(tgemv_kernel<NT>, dim3(grid), dim3(kTgThreads), TgCfg<NT>::kSmem, st, tw, tx, p);
+    return launch_k(tgemv_kernel<NT>, dim3(grid), dim3(TgCfg<NT>::kThreads), TgCfg<NT>::kSmem, st, tw, tx, p);
 }
 
 }  // namespace
