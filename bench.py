@@ -317,8 +317,11 @@ def run_mine(args) -> None:
     api = Agsv()
 
     def cfg_of(policy, profile_kernels=False):
-        return workloads.run_config(args.config, clock=clock, policy=policy, n_shards=n_gpus, shard=rank,
-                                    device=dev_idx, profile_kernels=profile_kernels)
+        c = workloads.run_config(args.config, clock=clock, policy=policy, n_shards=n_gpus, shard=rank,
+                                 device=dev_idx, profile_kernels=profile_kernels)
+        if args.horizon_ms:  # profiling runs only (ncu launch lists): cut every episode
+            c["horizon_ms"] = args.horizon_ms
+        return c
 
     cfg = cfg_of(args.policy)
     td = tempfile.mkdtemp()
@@ -536,6 +539,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU slice for cpu_baseline")
     ap.add_argument("--ref-budget", type=float, default=150.0, help="reference arm: total CPU seconds over all steps")
+    ap.add_argument("--horizon-ms", type=float, default=None,
+                    help="cut every episode at this engine time (ncu launch-list captures only; not a bench line)")
     args = ap.parse_args()
     if args.warmup < 3 and not args.virtual:
         args.warmup = 3
