@@ -122,7 +122,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const size_t pbase = units ? static_cast<size_t>(unit.w < 0 ? 0 : unit.w) * gridDim.y + kvh
                                : (static_cast<size_t>(item_idx) * gridDim.y + kvh) * gridDim.z + blockIdx.z;
     if (n_kv == 0) {
-        // empty split: neutral partials
+        // empty split: neutral partials (after the PDL wait: the previous layer's combine may
+        // still be reading this partial slot)
+        pdl_trigger();
+        pdl_wait();
         for (int r = threadIdx.x; r < 256; r += blockDim.x) {
             part_ml[(pbase * 256 + r) * 2 + 0] = -FLT_MAX;
             part_ml[(pbase * 256 + r) * 2 + 1] = 0.f;

@@ -45,6 +45,8 @@ struct AttnShape {
     float scale_log2; // log2(e) / sqrt(hd)
     unsigned long long* dbg = nullptr;  // decode attention: per-CTA globaltimer stamps [cta][8]
     int dbg_load_only = 0;  // decode attention timing ablation: consumers skip the math
+    int no_prewait = 0;     // decode attention: wait for the previous kernel before any block
+                            // (ASB_ATTN_PREWAIT=0; default streams blocks older than this step first)
 };
 
 // grid = (items, hkv, splits).  Split-KV over gridDim.z when the grid is small (resume

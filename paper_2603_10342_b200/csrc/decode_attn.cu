@@ -192,11 +192,14 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         // running, and wait for it only before the block that holds the new token.
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            const int new_page = it.pad / kBlockTokens;  // first block this step writes
+            const int new_page = s.no_prewait ? 0 : it.pad / kBlockTokens;  // first block this step writes
             bool waited = false;
             for (int i = 0; i < n_local; ++i) {
                 if (!waited && p0 + i >= new_page) {
                     pdl_wait();
+                    // the QKV kernel wrote this step's K/V with generic stores; the blocks are read
+                    // by TMA (async proxy)
+                    fence_proxy_async_global();
                     waited = true;
                 }
                 const int st = i % kStagesR;
@@ -498,7 +501,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                 const DecodeItem it = items[item];
                 const int n_pages = (it.ctx_len + kBlockTokens - 1) / kBlockTokens;
                 const int p0 = sp * pps, n_local = max(0, min(n_pages, p0 + pps) - p0);
-                const int new_page = it.pad / kBlockTokens;  // first block this step writes
+                const int new_page = s.no_prewait ? 0 : it.pad / kBlockTokens;  // first block this step writes
                 const int32_t* table = tables + it.table_off;
                 for (int i = 0; i < n_local; ++i, ++gi) {
                     // only the block holding this step's token depends on the kernel before us
@@ -610,6 +613,8 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                 }
             }
             named_sync(1, kWarps * 32);  // done with the held block
+            fence_proxy_async_smem();    // the merge scratch's generic writes before the next TMA
+            __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
         } else if (tid < G) {
             // an empty split (ragged contexts): contributes nothing to the merge
@@ -716,7 +721,7 @@ cudaError_t launch_hd(const CUtensorMap& tkv, const __nv_bfloat16* q, const Deco
         a[0].val.clusterDim.y = 1;
         a[0].val.clusterDim.z = splits;
         int na = 1;
-        if (tl_pdl) {
+        if (pdl_for_launch(true)) {
             a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
             a[1].val.programmaticStreamSerializationAllowed = 1;
             na = 2;

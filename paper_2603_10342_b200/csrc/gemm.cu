@@ -35,6 +35,7 @@
 #include "attn.h"
 #include "epi.cuh"
 #include "gemm.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace asb {
@@ -928,7 +929,8 @@ cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const GemmPa
         attr[na].val.clusterDim.z = 1;
         ++na;
     }
-    if (pdl) {
+    const bool use_pdl = pdl_for_launch(clustered) && pdl;  // launch.cuh: no PDL right after a cluster launch
+    if (use_pdl) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;

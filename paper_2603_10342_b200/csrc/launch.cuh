@@ -6,6 +6,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <utility>
 
 namespace asb {
@@ -13,6 +14,22 @@ namespace asb {
 // Per host thread: whether launches issued now carry the PDL attribute (set by asb_forward
 // for the duration of one forward; off while per-launch profiling events are recorded).
 inline thread_local bool tl_pdl = false;
+
+// Whether the previous launch on this host thread was a thread-block-cluster launch.  A kernel
+// launched programmatically (PDL) right after a cluster launch is launched WITHOUT the attribute:
+// its griddepcontrol.wait did not reliably order it after the cluster grid's stores here (the
+// decode step was run-to-run nondeterministic when the fused QKV GEMM ran as S-CTA split-K
+// clusters; deterministic with the same kernels and no PDL, or with single-CTA tiles:
+// scripts/determinism.py, profiles/r2_pdl_cluster_determinism.txt).  ASB_PDL_AFTER_CLUSTER=1
+// restores PDL there (A/B only).
+inline thread_local bool tl_prev_cluster = false;
+inline bool pdl_for_launch(bool is_cluster) {
+    static const bool after_cluster = std::getenv("ASB_PDL_AFTER_CLUSTER") &&
+                                      std::atoi(std::getenv("ASB_PDL_AFTER_CLUSTER")) != 0;
+    const bool use = tl_pdl && (after_cluster || !tl_prev_cluster);
+    tl_prev_cluster = is_cluster;
+    return use;
+}
 
 struct PdlScope {
     bool prev;
@@ -29,7 +46,7 @@ cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
-    if (tl_pdl) {
+    if (pdl_for_launch(false)) {
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;

@@ -1146,6 +1146,8 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
             static const bool load_only = std::getenv("ASB_DEBUG_SKIP") &&
                                           std::string(std::getenv("ASB_DEBUG_SKIP")).find("attnmath") != std::string::npos;
             as.dbg_load_only = load_only ? 1 : 0;
+            static const bool no_prewait = std::getenv("ASB_ATTN_PREWAIT") && std::atoi(std::getenv("ASB_ATTN_PREWAIT")) == 0;
+            as.no_prewait = no_prewait ? 1 : 0;
         }
         if (L->attn_dbg) {
             cuda_check(cudaMemsetAsync(L->attn_dbg, 0, 1024 * 8 * 8, L->stream), "attn dbg");

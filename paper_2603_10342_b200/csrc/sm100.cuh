@@ -124,6 +124,9 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 
 // Generic-proxy smem writes -> visible to the async proxy (tcgen05.mma / TMA store).
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

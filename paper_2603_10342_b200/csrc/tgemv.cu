@@ -221,6 +221,8 @@ __global__ void __launch_bounds__(TgCfg<NT>::kThreads, 1)
                 }
                 named_sync(1, kTgWarps * 32);
                 if (!s_last) {
+                    fence_proxy_async_smem();  // generic writes (red) before the next TMA into the stage
+                    __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[st_last]);
                     continue;
                 }
@@ -311,6 +313,8 @@ __global__ void __launch_bounds__(TgCfg<NT>::kThreads, 1)
             }
             }
             named_sync(1, kTgWarps * 32);  // every warp is done with red: release the stage
+            fence_proxy_async_smem();       // order red's generic writes before the next TMA write
+            __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st_last]);
         }
     }

@@ -1,0 +1,8 @@
+run() { timeout 300 python scripts/kernel_bench.py --no-prefill "$@" --out /tmp/k.json 2>&1 | python3 -c "
+import sys,json
+for l in sys.stdin:
+    try: d=json.loads(l)
+    except Exception: print(l.strip()[:200]); continue
+    print(d['model'], d['case'], 'sms', d['sms'], 'attn %.1f us/layer %.0f GB/s' % (d['decode_attn_us_per_layer'], d['decode_attn_gbs']), 'step %.3f' % d['step_ms_unprofiled'])
+"; }
+for env in "X=0" "ASB_ATTN_NO_CLUSTER=1" "ASB_ATTN_PREWAIT=0"; do echo "=== $env"; env $env bash -c "$(declare -f run); run --models llama3.2-3b --decode 2x3000 8x3000 32x3000; run --models qwen2.5-7b llama3.1-8b; run --models llama3.2-3b --decode 8x3000 16x3000 --level 2"; done
