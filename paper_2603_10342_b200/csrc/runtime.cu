@@ -427,7 +427,7 @@ void tgemv_buffers(asb_lane* L) {
 // has enough 128-row tiles for one whole wave (no K split); the tcgen05 kernel keeps 17-32
 // tokens (tgemv is MMA-issue bound there: 256 m16n8k16 per 32 KiB stage) and the small 0.5B
 // projections.  ASB_NO_TGEMV=1: never (A/B baseline); ASB_TGEMV=1: every T <= 32 linear.
-bool use_tgemv(int T, const Weight& w, int num_sms) {
+bool use_tgemv(int T, const Weight& w, int num_sms, int epi) {
     static const int mode = std::getenv("ASB_NO_TGEMV") && std::atoi(std::getenv("ASB_NO_TGEMV")) != 0 ? 0
                             : std::getenv("ASB_TGEMV") && std::atoi(std::getenv("ASB_TGEMV")) != 0     ? 2
                                                                                                         : 1;
@@ -435,7 +435,11 @@ bool use_tgemv(int T, const Weight& w, int num_sms) {
     if (mode == 2) return true;
     const double bytes = 2.0 * double(w.rows) * w.cols;
     const int tiles = w.rows_pad / 128;
-    return T <= 16 && bytes >= 16e6 && w.cols >= 2048 && (num_sms <= 120 || tiles * 5 >= num_sms * 4);
+    if (T <= 16) return bytes >= 16e6 && w.cols >= 2048 && (num_sms <= 120 || tiles * 5 >= num_sms * 4);
+    // 17-32 tokens (decode steps carrying an admitted-resume chunk): only the fused QKV projection
+    // on a 40-72 SM partition, where the tcgen05 kernel splits its few tiles over clusters
+    // (1.17-1.28x there; the other projections stay on tcgen05, profiles/r2_tgemv_17_32.txt)
+    return epi == EPI_QKV && bytes >= 16e6 && num_sms >= 40 && num_sms <= 72 && tiles < num_sms;
 }
 
 // Y[T][n_out] = X[T][k] . W^T with the path chosen by T (path 2 = dgemv, 3 = tgemv, 1 = tcgen05
@@ -476,7 +480,7 @@ void linear(asb_lane* L, const XIn& xin, const Weight& w, int T, int epi,
         return;
     }
     if (xin.norm_w || xin.rows) fail(ASB_ERR_INVALID_ARGUMENT, "fused norm / row gather needs the dgemv path");
-    if (force_path == 3 || (force_path < 0 && use_tgemv(T, w, L->n_sms()))) {
+    if (force_path == 3 || (force_path < 0 && use_tgemv(T, w, L->n_sms(), epi))) {
         if (T > 32) fail(ASB_ERR_INVALID_ARGUMENT, "tgemv takes <= 32 tokens");
         tgemv_buffers(L);
         TgemvParams d{};

@@ -168,7 +168,9 @@ def test_full_width_truncated_matches_oracle(case):
     {"ASB_PREFILL_UNITS": "0"},
     {"ASB_PREFILL_UNITS": "0", "ASB_PREFILL_SPLITS": "3"},
     {"ASB_DECODE_PERSIST": "1"},
-], ids=["cluster3", "last_arriver16", "combine", "single", "prefill_uniform", "prefill_uniform3", "persistent"])
+    {"ASB_TGEMV": "1"},
+], ids=["cluster3", "last_arriver16", "combine", "single", "prefill_uniform", "prefill_uniform3", "persistent",
+        "tgemv_all"])
 def test_c4_layout_merge_paths(env):
     e = dict(os.environ)
     e.update(env)
