@@ -72,6 +72,11 @@ SLACK = 1.5
 # the complementary partition prefills (C3 episodes: 48-SM steps 4.4-5.0 ms in-episode at the
 # batch the profile measures in isolation at 4.1-4.2 ms, profiles/r2_chunk_as_decode.txt)
 CORUN = 1.1
+# prefill launch unit (tokens of a Q_P job per forward): 4096 fills whole waves of the prefill
+# GEMMs far better than 2048 (e.g. 3B o/down: 384 vs 192 tiles on 148 SMs, 86% vs 65% fill;
+# profiles/r2_prefill_gemm_waves.txt): C3 TTFT p99 -25% and +3% tokens/s for both policies
+# (profiles/r2_policy_compare_c3_unit{2,3,4}.json)
+UNIT_TOKENS = 4096
 
 
 def profile_path(model: str) -> Path:
@@ -113,7 +118,7 @@ def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_fra
 def run_config(name: str, *, clock: str = "wall", policy: str = "agentserve", n_shards: int = 1,
                shard: int = 0, device: int = 0, profile_kernels: bool = False, lend: bool = True,
                calibrated: bool = True, slack: float = SLACK, theta_low_frac: float = 0.5,
-               static_slots: int | None = None, unit_tokens: int = 2048, seed: int = 13) -> dict:
+               static_slots: int | None = None, unit_tokens: int = UNIT_TOKENS, seed: int = 13) -> dict:
     """agsv_* run config of one BASELINE configuration.  n_shards > 1: this replica serves the
     sessions gid % n_shards == shard of the global agents*n_shards-session workload."""
     c = CONFIGS[name]

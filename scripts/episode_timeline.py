@@ -27,7 +27,7 @@ pol, kw = parse_spec(a.spec)
 cfg = workloads.run_config(a.config, clock=a.clock, policy=pol, lend=bool(kw.get("lend", 1)),
                            calibrated=bool(kw.get("calib", 1)), slack=float(kw.get("slack", workloads.SLACK)),
                            theta_low_frac=float(kw.get("tlow", 0.5)), static_slots=kw.get("k"),
-                           unit_tokens=int(kw.get("unit", 2048)))
+                           unit_tokens=int(kw.get("unit", workloads.UNIT_TOKENS)))
 for key, ck in (("dt", "delta_t_ms"), ("r0", "initial_r_slots"), ("rbase", "r_base_slots")):
     if key in kw:
         cfg.setdefault("controller", {})[ck] = kw[key]

@@ -11,7 +11,7 @@ attainment, rebind latency and the competitive-ratio verification summary.
 A run spec is policy[:key=value,...] with keys lend (0/1), slack, tlow (theta_low / tau),
 calib (0/1: measured-curve calibration vs the reference's factor-8), k (static decode slots),
 unit (prefill launch-unit tokens), dt (control interval ms), r0 / rbase (initial / base
-decode slots).
+decode slots), b0 / bmin (initial / minimum resume-prefill budget tokens).
 """
 import argparse
 import json
@@ -64,13 +64,17 @@ def run_spec(api, cfg_name, spec, reps, td, horizon=None):
     cfg = workloads.run_config(cfg_name, policy=pol, lend=bool(kw.get("lend", 1)),
                                calibrated=bool(kw.get("calib", 1)), slack=float(kw.get("slack", workloads.SLACK)),
                                theta_low_frac=float(kw.get("tlow", 0.5)),
-                               static_slots=kw.get("k"), unit_tokens=int(kw.get("unit", 2048)))
+                               static_slots=kw.get("k"), unit_tokens=int(kw.get("unit", workloads.UNIT_TOKENS)))
     if "dt" in kw:
         cfg.setdefault("controller", {})["delta_t_ms"] = float(kw["dt"])
     if "r0" in kw:
         cfg.setdefault("controller", {})["initial_r_slots"] = int(kw["r0"])
     if "rbase" in kw:
         cfg.setdefault("controller", {})["r_base_slots"] = int(kw["rbase"])
+    if "b0" in kw:
+        cfg.setdefault("controller", {})["initial_b_tokens"] = int(kw["b0"])
+    if "bmin" in kw:
+        cfg.setdefault("controller", {})["b_min_tokens"] = int(kw["bmin"])
     if horizon:
         cfg["horizon_ms"] = horizon
     gaps, ttft, tps, att, reb, ends, tokens = [], [], [], [], [], [], 0
