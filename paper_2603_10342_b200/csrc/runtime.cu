@@ -1090,8 +1090,11 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
             static const bool chunk_dec = !(std::getenv("ASB_CHUNK_AS_DECODE") &&
                                             std::atoi(std::getenv("ASB_CHUNK_AS_DECODE")) == 0);
             constexpr int kChunkAsDecode = 16;
-            if (g.n_tokens == 1 ||
-                (chunk_dec && g.n_tokens <= kChunkAsDecode && int(ditems.size()) + g.n_tokens <= L->max_ditems)) {
+            // (on small partitions the chunk rows' repeated K/V reads cost more per-SM streaming
+            // than the tensor-core path's one read per tile: decode rows only from 96 SMs,
+            // profiles/r2_chunk_as_decode.txt)
+            if (g.n_tokens == 1 || (chunk_dec && L->n_sms() >= 96 && g.n_tokens <= kChunkAsDecode &&
+                                    int(ditems.size()) + g.n_tokens <= L->max_ditems)) {
                 for (int t = 0; t < g.n_tokens; ++t) ditems.push_back(DecodeItem{row + t, start + t + 1, toff, start});
                 max_ctx = std::max(max_ctx, start + g.n_tokens);
                 dattn_seg_bytes += double(start + g.n_tokens) * s.hkv * s.hd * 2 * 2;  // K/V read once per session
