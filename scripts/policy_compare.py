@@ -122,8 +122,13 @@ def main():
         prof, _ = workloads.load_profile(workloads.CONFIGS[a.config]["model"])
         runs += [f"static_partition:k={k}" for k in range(1, prof["total_sms"] // prof["granularity"])]
     rows = []
+    sys.path.insert(0, str(ROOT))
+    from bench import ClockSampler  # nvidia-smi clocks / throttle reasons during each run
     for spec in runs:
+        sampler = ClockSampler(0)
+        sampler.start()
         row = run_spec(api, a.config, spec, a.reps, td, a.horizon_ms)
+        row["clocks"] = sampler.stop()
         rows.append(row)
         print(json.dumps(row), flush=True)
     doc = {"config": a.config, "label": workloads.CONFIGS[a.config]["label"], "reps": a.reps,
