@@ -95,6 +95,7 @@ def _oracle_check(recs, model="tiny"):
                     near += 1
                 expect[s] = sess[s].forward([tok])
     assert checked > 0
+    print(f"trace replay: {checked} greedy ids checked on the oracle, near-ties {near}")
     assert near <= max(1, checked // 20), (near, checked)
     return checked, near
 
