@@ -24,13 +24,20 @@ struct PrefillItem {
     int table_off;  // offset of this segment's block table in the batch table array
 };
 
-// One decode-attention row: a single query token.
+// One decode-attention item: up to 8 (token, query head) columns of one KV head's MMA N tile.
+// The columns of a token group (n tokens of one session at consecutive rows / positions:
+// a decode row is n = 1, an admitted resume chunk n <= 16) are numbered c = token * G + head;
+// an item takes columns col0 .. col0 + 7 of its group, so a chunk's tokens share each K/V block
+// read (G = 3: 16 tokens in 6 items instead of 16 single-token rows).
 struct DecodeItem {
-    int q_row;      // row in q / out
-    int ctx_len;    // keys to attend (positions 0..ctx_len-1), includes the row's own token
+    int q_row;      // row in q / out of the group's first token
+    int ctx_len;    // keys the first token attends (positions 0..ctx_len-1, its own included);
+                    // token j of the group attends ctx_len + j
     int table_off;  // block table offset
-    int pad;        // first position of the row's session written by this forward (its blocks
-                    // are read only after the QKV kernel: PDL wait); ctx_len - 1 for a decode row
+    int pad;        // first position of the session written by this forward (its blocks are
+                    // read only after the QKV kernel: PDL wait); ctx_len - 1 for a decode row
+    int col0;       // first column of this item within its group
+    int ncols;      // columns of the group (n * G); columns >= ncols are padding
 };
 
 // KV pool page layout: [layer][block][kv_head][K rows 0..63 | V rows 0..63][hd] bf16 -- the K and

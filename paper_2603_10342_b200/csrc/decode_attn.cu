@@ -69,11 +69,32 @@ __device__ __forceinline__ uint32_t kv_off(int kv, int r, int c) {
     return line * 128 + (((c & 7) ^ (r & 7)) << 4);
 }
 
+// Column c (0..7) of an item's MMA N tile: token j = (col0 + c) / G of its group, query head
+// (col0 + c) % G of the KV head's G, q / out row q_row + j, keys 0 .. ctx_len + j - 1 (lim 0:
+// a padding column, everything masked)
+struct DCol {
+    int row, head, lim;
+};
+__device__ __forceinline__ DCol dcol(const DecodeItem& it, int c, int G) {
+    const int cc = it.col0 + c;
+    const int j = cc / G;
+    DCol d;
+    d.row = it.q_row + j;
+    d.head = cc - j * G;
+    d.lim = cc < it.ncols ? it.ctx_len + j : 0;
+    return d;
+}
+// keys of the item's last column: the block range it streams
+__device__ __forceinline__ int item_keys(const DecodeItem& it, int G) {
+    return it.ctx_len + min(it.col0 + 7, it.ncols - 1) / G;
+}
+__device__ __forceinline__ int item_cols(const DecodeItem& it) { return min(8, it.ncols - it.col0); }
+
 // One 64-token K|V block of the online softmax for this warp's 16 keys (kw..kw+15 of the
 // block, absolute key index kbase + ..): S^T = K Q^T, running max / sum per head column,
 // O^T = alpha O^T + V^T P^T.
 template <int HD>
-__device__ __forceinline__ void attn_page(uint32_t base, int kw, int kbase, int ctx_len, const uint32_t (&qb)[HD / 16][2],
+__device__ __forceinline__ void attn_page(uint32_t base, int kw, int kbase, const int (&lim)[2], const uint32_t (&qb)[HD / 16][2],
                                           float (&o)[HD / 16][4], float (&m_run)[2], float (&l_run)[2],
                                           float scale_log2, int lane) {
     constexpr int MT = HD / 16;
@@ -90,12 +111,11 @@ __device__ __forceinline__ void attn_page(uint32_t base, int kw, int kbase, int 
             else mma16816(sa, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
         }
     }
-    // ---- online softmax per head column: values (key g | g+8, head 2t + j)
-    const bool ok0 = kbase + g < ctx_len, ok1 = kbase + g + 8 < ctx_len;
+    // ---- online softmax per column: values (key g | g+8, column 2t + j), causal per column
     float sv[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-        const bool ok = e < 2 ? ok0 : ok1;
+        const bool ok = kbase + g + (e < 2 ? 0 : 8) < lim[e & 1];
         sv[e] = ok ? (sa[e] + sb[e]) * scale_log2 : -FLT_MAX;
     }
     float alpha[2], mx[2];
@@ -169,7 +189,8 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     const int kvh = blockIdx.y;
     const int G = s.hq / s.hkv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_pages = (it.ctx_len + kBlockTokens - 1) / kBlockTokens;
+    const int NC = item_cols(it);  // live columns of this item
+    const int n_pages = (item_keys(it, G) + kBlockTokens - 1) / kBlockTokens;
     const int p0 = blockIdx.z * pages_per_split;
     const int n_local = max(0, min(n_pages, p0 + pages_per_split) - p0);
     const int32_t* table = tables + it.table_off;
@@ -222,10 +243,11 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     // 16-dim k-step; heads >= G are zero columns
     uint32_t qb[HD / 16][2];
     {
-        const __nv_bfloat16* qrow = q + (size_t)it.q_row * s.hq * HD + (size_t)(kvh * G + g) * HD;
+        const DCol qc = dcol(it, g, G);
+        const __nv_bfloat16* qrow = q + (size_t)qc.row * s.hq * HD + (size_t)(kvh * G + qc.head) * HD;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-            if (g < G) {
+            if (qc.lim > 0) {
                 qb[kk][0] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t);
                 qb[kk][1] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t + 8);
             } else {
@@ -233,6 +255,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             }
         }
     }
+    const int lim[2] = {dcol(it, 2 * t, G).lim, dcol(it, 2 * t + 1, G).lim};  // this thread's columns
     // O^T accumulators: m-tile mt holds (dim mt*16+g, heads 2t, 2t+1) and (dim +8, same heads)
     float o[MT][4];
 #pragma unroll
@@ -249,7 +272,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             if (lane == 0) mbar_arrive(&empty[st]);
             continue;
         }
-        attn_page<HD>(smem_u32(ring + st * C::kStage), kw, (p0 + i) * kBlockTokens + kw, it.ctx_len, qb, o, m_run,
+        attn_page<HD>(smem_u32(ring + st * C::kStage), kw, (p0 + i) * kBlockTokens + kw, lim, qb, o, m_run,
                       l_run, s.scale_log2, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
@@ -268,8 +291,8 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     float* mw = mrg + warp * 8 * HD;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-        const int h = 2 * t + j;
-        if (h < G) {
+        const int h = 2 * t + j;  // column
+        if (h < NC) {
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
                 mw[h * HD + mt * 16 + g] = o[mt][j];
@@ -285,10 +308,10 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     const bool single = gridDim.z == 1;
     const bool cmerge = !single && cluster_merge;
     // cluster merge: this CTA's (M, L, O) parked at the start of the drained ring
-    float* cO = mrg + kWarps * 8 * HD;           // [G][HD], behind the warp records
-    float* cM = cO + 8 * HD;                     // [G]
-    float* cL = cM + 8;                          // [G]
-    for (int e = threadIdx.x; e < G * HD; e += kWarps * 32) {
+    float* cO = mrg + kWarps * 8 * HD;           // [column][HD], behind the warp records
+    float* cM = cO + 8 * HD;                     // [column]
+    float* cL = cM + 8;                          // [column]
+    for (int e = threadIdx.x; e < NC * HD; e += kWarps * 32) {
         const int h = e / HD, d = e % HD;
         float M = -FLT_MAX;
 #pragma unroll
@@ -302,9 +325,9 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             L += lw * f;
             O += mrg[(w * 8 + h) * HD + d] * f;
         }
-        const int hh = kvh * G + h;
         if (single) {
-            out[(size_t)it.q_row * s.hq * HD + hh * HD + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+            const DCol oc = dcol(it, h, G);
+            out[(size_t)oc.row * s.hq * HD + (kvh * G + oc.head) * HD + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
         } else if (cmerge) {
             cO[h * HD + d] = O;
             if (d == 0) {
@@ -312,7 +335,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                 cL[h] = L;
             }
         } else {
-            const size_t slot = ((size_t)blockIdx.x * s.hq + hh) * gridDim.z + blockIdx.z;
+            const size_t slot = (((size_t)blockIdx.x * s.hkv + kvh) * 8 + h) * gridDim.z + blockIdx.z;
             part_o[slot * HD + d] = O;
             if (d == 0) {
                 part_ml[slot * 2 + 0] = M;
@@ -333,7 +356,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         cluster_sync();
         if (threadIdx.x == 0) stamp(4);
         const int S = gridDim.z, r = blockIdx.z;
-        const int n = G * HD, lo = (n * r) / S, hi = (n * (r + 1)) / S;
+        const int n = NC * HD, lo = (n * r) / S, hi = (n * (r + 1)) / S;
         const uint32_t bO = smem_u32(cO), bM = smem_u32(cM), bL = smem_u32(cL);
         for (int e = lo + threadIdx.x; e < hi; e += kWarps * 32) {
             const int h = e / HD, d = e % HD;
@@ -358,7 +381,8 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                 L += lq[q] * w;
                 O += oq[q] * w;
             }
-            out[(size_t)it.q_row * s.hq * HD + (kvh * G + h) * HD + d] = __float2bfloat16_rn(O / L);
+            const DCol oc = dcol(it, h, G);
+            out[(size_t)oc.row * s.hq * HD + (kvh * G + oc.head) * HD + d] = __float2bfloat16_rn(O / L);
         }
         cluster_sync();  // peers may still be reading this CTA's partial
         if (threadIdx.x == 0) stamp(5);
@@ -383,17 +407,18 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     // per (head, split) weight exp2(m - M) and the normaliser L, once per head, in smem (the
     // ring is drained); then one pass over part_o with every split's load in flight
     const int splits = gridDim.z;
-    float* wsp = reinterpret_cast<float*>(smem);  // [G][splits]
-    float* linv = wsp + 8 * splits;               // [G]
-    float* lsp = linv + 8;  // [G][splits] l
-    for (int i = threadIdx.x; i < G * splits; i += kWarps * 32) {  // all (m, l) loads at once
+    float* wsp = reinterpret_cast<float*>(smem);  // [column][splits]
+    float* linv = wsp + 8 * splits;               // [column]
+    float* lsp = linv + 8;  // [column][splits] l
+    const size_t slot0 = ((size_t)blockIdx.x * s.hkv + kvh) * 8;  // column h: (slot0 + h) * splits + split
+    for (int i = threadIdx.x; i < NC * splits; i += kWarps * 32) {  // all (m, l) loads at once
         const int h = i / splits, sp = i % splits;
-        const size_t sl = ((size_t)blockIdx.x * s.hq + kvh * G + h) * splits + sp;
+        const size_t sl = (slot0 + h) * splits + sp;
         wsp[i] = __ldcg(part_ml + sl * 2);
         lsp[i] = __ldcg(part_ml + sl * 2 + 1);
     }
     named_sync(1, kWarps * 32);
-    if (threadIdx.x < G) {
+    if (threadIdx.x < NC) {
         float M = -FLT_MAX;
         for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, wsp[threadIdx.x * splits + sp]);
         float L = 0.f;
@@ -406,10 +431,9 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         linv[threadIdx.x] = L;
     }
     named_sync(1, kWarps * 32);
-    for (int e = threadIdx.x; e < G * HD; e += kWarps * 32) {
+    for (int e = threadIdx.x; e < NC * HD; e += kWarps * 32) {
         const int h = e / HD, d = e % HD;
-        const int hh = kvh * G + h;
-        const float* po = part_o + ((size_t)blockIdx.x * s.hq + hh) * splits * HD + d;
+        const float* po = part_o + (slot0 + h) * splits * HD + d;
         // every split's load in flight at once (splits <= 16), then the weighted sum in order
         float pv[16];
 #pragma unroll
@@ -420,21 +444,25 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             const float w = sp < splits ? wsp[h * splits + sp] : 0.f;
             if (w != 0.f) O += pv[sp] * w;
         }
-        out[(size_t)it.q_row * s.hq * HD + hh * HD + d] = __float2bfloat16_rn(O / linv[h]);
+        const DCol oc = dcol(it, h, G);
+        out[(size_t)oc.row * s.hq * HD + (kvh * G + oc.head) * HD + d] = __float2bfloat16_rn(O / linv[h]);
     }
     if (threadIdx.x == 0) stamp(5);
 }
 
-// Merge split partials -> normalised bf16 output.  grid = (n_items, hq), block = HD.
+// Merge split partials -> normalised bf16 output.  grid = (n_items, hkv * 8 columns), block = HD.
 template <int HD>
 __global__ void decode_combine_kernel(const DecodeItem* __restrict__ items,
                                       const float* __restrict__ part_o,
                                       const float* __restrict__ part_ml, int splits,
-                                      __nv_bfloat16* __restrict__ out, int hq) {
+                                      __nv_bfloat16* __restrict__ out, int hq, int hkv) {
     pdl_trigger();
     pdl_wait();
-    const int row = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
-    const size_t base = ((size_t)row * hq + h) * splits;
+    const int row = blockIdx.x, kvh = blockIdx.y / 8, c = blockIdx.y % 8, d = threadIdx.x;
+    const DecodeItem it = items[row];
+    if (c >= item_cols(it)) return;
+    const int G = hq / hkv;
+    const size_t base = (((size_t)row * hkv + kvh) * 8 + c) * splits;
     float M = -FLT_MAX;
     for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, part_ml[(base + sp) * 2]);
     float L = 0.f, O = 0.f;
@@ -445,7 +473,8 @@ __global__ void decode_combine_kernel(const DecodeItem* __restrict__ items,
         L += ls * w;
         O += part_o[(base + sp) * HD + d] * w;
     }
-    out[(size_t)items[row].q_row * hq * HD + h * HD + d] = __float2bfloat16_rn(O / L);
+    const DCol oc = dcol(it, c, G);
+    out[(size_t)oc.row * hq * HD + (kvh * G + oc.head) * HD + d] = __float2bfloat16_rn(O / L);
 }
 
 // Persistent form for grids of more than one wave (small Green Context partitions): one wave
@@ -499,7 +528,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 const int item = u / (s.hkv * splits), kvh = (u / splits) % s.hkv, sp = u % splits;
                 const DecodeItem it = items[item];
-                const int n_pages = (it.ctx_len + kBlockTokens - 1) / kBlockTokens;
+                const int n_pages = (item_keys(it, G) + kBlockTokens - 1) / kBlockTokens;
                 const int p0 = sp * pps, n_local = max(0, min(n_pages, p0 + pps) - p0);
                 const int new_page = s.no_prewait ? 0 : it.pad / kBlockTokens;  // first block this step writes
                 const int32_t* table = tables + it.table_off;
@@ -530,14 +559,16 @@ __global__ void __launch_bounds__(kThreadsD, 2)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int item = u / (s.hkv * splits), kvh = (u / splits) % s.hkv, sp = u % splits;
         const DecodeItem it = items[item];
-        const int n_pages = (it.ctx_len + kBlockTokens - 1) / kBlockTokens;
+        const int NC = item_cols(it);
+        const int n_pages = (item_keys(it, G) + kBlockTokens - 1) / kBlockTokens;
         const int p0 = sp * pps, n_local = max(0, min(n_pages, p0 + pps) - p0);
         uint32_t qb[HD / 16][2];
         {
-            const __nv_bfloat16* qrow = q + (size_t)it.q_row * s.hq * HD + (size_t)(kvh * G + g) * HD;
+            const DCol qc = dcol(it, g, G);
+            const __nv_bfloat16* qrow = q + (size_t)qc.row * s.hq * HD + (size_t)(kvh * G + qc.head) * HD;
 #pragma unroll
             for (int kk = 0; kk < HD / 16; ++kk) {
-                if (g < G) {
+                if (qc.lim > 0) {
                     qb[kk][0] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t);
                     qb[kk][1] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t + 8);
                 } else {
@@ -549,12 +580,13 @@ __global__ void __launch_bounds__(kThreadsD, 2)
 #pragma unroll
         for (int n = 0; n < MT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
         float m_run[2] = {-FLT_MAX, -FLT_MAX}, l_run[2] = {0.f, 0.f};
+        const int lim[2] = {dcol(it, 2 * t, G).lim, dcol(it, 2 * t + 1, G).lim};
         int st = 0;
         for (int i = 0; i < n_local; ++i, ++gi) {
             st = gi % kS;
             mbar_wait(&full[st], (gi / kS) & 1);
             if (!s.dbg_load_only)
-                attn_page<HD>(smem_u32(ring + st * C::kStage), kw, (p0 + i) * kBlockTokens + kw, it.ctx_len, qb, o,
+                attn_page<HD>(smem_u32(ring + st * C::kStage), kw, (p0 + i) * kBlockTokens + kw, lim, qb, o,
                               m_run, l_run, s.scale_log2, lane);
             __syncwarp();
             if (lane == 0 && i + 1 < n_local) mbar_arrive(&empty[st]);
@@ -565,7 +597,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             l_run[j] += __shfl_xor_sync(0xffffffffu, l_run[j], 8);
             l_run[j] += __shfl_xor_sync(0xffffffffu, l_run[j], 16);
         }
-        const size_t slot0 = ((size_t)item * s.hq + kvh * G) * splits + sp;  // head h: slot0 + h * splits
+        const size_t slot0 = ((size_t)item * s.hkv + kvh) * 8 * splits + sp;  // column h: slot0 + h * splits
         if (n_local > 0) {
             // ---- merge the warps through the held block, then this unit's output
             float* mrg = reinterpret_cast<float*>(ring + st * C::kStage);  // [warp][8][HD]
@@ -573,8 +605,8 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             float* mw = mrg + warp * 8 * HD;
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                const int h = 2 * t + j;
-                if (h < G) {
+                const int h = 2 * t + j;  // column
+                if (h < NC) {
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
                         mw[h * HD + mt * 16 + g] = o[mt][j];
@@ -587,7 +619,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                 }
             }
             named_sync(1, kWarps * 32);
-            for (int e = tid; e < G * HD; e += kWarps * 32) {
+            for (int e = tid; e < NC * HD; e += kWarps * 32) {
                 const int h = e / HD, d = e % HD;
                 float M = -FLT_MAX;
 #pragma unroll
@@ -602,7 +634,9 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                     O += mrg[(w * 8 + h) * HD + d] * f;
                 }
                 if (splits == 1) {
-                    out[(size_t)it.q_row * s.hq * HD + (kvh * G + h) * HD + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+                    const DCol oc = dcol(it, h, G);
+                    out[(size_t)oc.row * s.hq * HD + (kvh * G + oc.head) * HD + d] =
+                        __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
                 } else {
                     const size_t sl = slot0 + (size_t)h * splits;
                     part_o[sl * HD + d] = O;
@@ -616,7 +650,7 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             fence_proxy_async_smem();    // the merge scratch's generic writes before the next TMA
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
-        } else if (tid < G) {
+        } else if (tid < NC) {
             // an empty split (ragged contexts): contributes nothing to the merge
             const size_t sl = slot0 + (size_t)tid * splits;
             part_ml[sl * 2 + 0] = -FLT_MAX;
@@ -635,14 +669,14 @@ __global__ void __launch_bounds__(kThreadsD, 2)
         named_sync(1, kWarps * 32);
         if (!s_last) continue;
         __threadfence();
-        for (int i = tid; i < G * splits; i += kWarps * 32) {
+        for (int i = tid; i < NC * splits; i += kWarps * 32) {
             const int h = i / splits, q2 = i % splits;
-            const size_t sl = ((size_t)item * s.hq + kvh * G + h) * splits + q2;
+            const size_t sl = slot0 - sp + ((size_t)h * splits + q2);
             wsp[h * 16 + q2] = __ldcg(part_ml + sl * 2);
             lsp[h * 16 + q2] = __ldcg(part_ml + sl * 2 + 1);
         }
         named_sync(1, kWarps * 32);
-        if (tid < G) {
+        if (tid < NC) {
             float M = -FLT_MAX;
             for (int q2 = 0; q2 < splits; ++q2) M = fmaxf(M, wsp[tid * 16 + q2]);
             float L = 0.f;
@@ -655,9 +689,9 @@ __global__ void __launch_bounds__(kThreadsD, 2)
             linv[tid] = L;
         }
         named_sync(1, kWarps * 32);
-        for (int e = tid; e < G * HD; e += kWarps * 32) {
+        for (int e = tid; e < NC * HD; e += kWarps * 32) {
             const int h = e / HD, d = e % HD;
-            const float* po = part_o + (((size_t)item * s.hq + kvh * G + h) * splits) * HD + d;
+            const float* po = part_o + (slot0 - sp + (size_t)h * splits) * HD + d;
             float pv[16];
 #pragma unroll
             for (int q2 = 0; q2 < 16; ++q2) pv[q2] = q2 < splits ? __ldcg(po + (size_t)q2 * HD) : 0.f;
@@ -667,7 +701,8 @@ __global__ void __launch_bounds__(kThreadsD, 2)
                 const float w = q2 < splits ? wsp[h * 16 + q2] : 0.f;
                 if (w != 0.f) O += pv[q2] * w;
             }
-            out[(size_t)it.q_row * s.hq * HD + (kvh * G + h) * HD + d] = __float2bfloat16_rn(O / linv[h]);
+            const DCol oc = dcol(it, h, G);
+            out[(size_t)oc.row * s.hq * HD + (kvh * G + oc.head) * HD + d] = __float2bfloat16_rn(O / linv[h]);
         }
         named_sync(1, kWarps * 32);  // wsp / mls reused by the next unit
     }
@@ -734,8 +769,8 @@ cudaError_t launch_hd(const CUtensorMap& tkv, const __nv_bfloat16* q, const Deco
     e = launch_k(decode_attn_kernel<HD>, grid, dim3(kThreadsD), smem, st, tkv, q, items, tables, out, po, pml,
                  cnt, pps, 0, s);
     if (e == cudaSuccess && splits > 1 && !cnt)
-        e = launch_k(decode_combine_kernel<HD>, dim3(n_items, s.hq), dim3(HD), 0, st, items,
-                     static_cast<const float*>(po), static_cast<const float*>(pml), splits, out, s.hq);
+        e = launch_k(decode_combine_kernel<HD>, dim3(n_items, s.hkv * 8), dim3(HD), 0, st, items,
+                     static_cast<const float*>(po), static_cast<const float*>(pml), splits, out, s.hq, s.hkv);
     return e;
 }
 

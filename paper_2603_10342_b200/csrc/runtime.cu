@@ -370,6 +370,7 @@ namespace {
 // boxes of 32/64 rows (swap-path B with two k-blocks per stage), [7] k-pair box of 16 rows
 // (tgemv at <= 16 tokens)
 constexpr int kActMaps = 8;
+constexpr int kDItemInts = int(sizeof(DecodeItem) / 4);  // DecodeItem slots in the meta block
 void act_maps(CUtensorMap* maps, const void* base, int rows, int cols) {
     const int boxes[5] = {128, 32, 64, 128, 256};
     for (int i = 0; i < 5; ++i)
@@ -915,14 +916,15 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->logits = static_cast<float*>(dmalloc(size_t(L->max_segs) * s.vocab * 4, L->allocs));
         if (std::getenv("ASB_GEMM_TIMELINE"))
             L->dbg_times = static_cast<unsigned long long*>(dmalloc(148 * 8 * 8, L->allocs));
-        // decode-attention rows: every single-token row plus the tokens of short segments (the
-        // admitted resume chunk of a decode step), each of which is its own causal decode row
+        // decode-attention items: one per single-token row, ceil(n * G / 8) per short segment (the
+        // admitted resume chunk of a decode step, its tokens' columns packed 8 per item); split
+        // partials per (item, kv head, column)
         L->max_ditems = std::min(T, L->max_segs + 32);
         const int dec_rows = L->max_ditems;
         L->part_o = static_cast<float*>(
-            dmalloc(size_t(dec_rows) * s.hq * L->max_splits * s.hd * 4, L->allocs));
+            dmalloc(size_t(dec_rows) * s.hkv * 8 * L->max_splits * s.hd * 4, L->allocs));
         L->part_ml = static_cast<float*>(
-            dmalloc(size_t(dec_rows) * s.hq * L->max_splits * 2 * 4, L->allocs));
+            dmalloc(size_t(dec_rows) * s.hkv * 8 * L->max_splits * 2 * 4, L->allocs));
         L->dcnt = static_cast<int*>(dmalloc(size_t(dec_rows) * s.hkv * 4, L->allocs));
         L->post_cnt = static_cast<int*>(dmalloc(64, L->allocs));
         tgemv_buffers(L.get());
@@ -938,7 +940,7 @@ asb_status asb_lane_create(asb_model* m, int max_tokens, int max_segments, void*
         L->ppart_rows = size_t(4096) * 256 / 4;
         L->ppart_o = static_cast<float*>(dmalloc(L->ppart_rows * s.hd * 4, L->allocs));
         L->ppart_ml = static_cast<float*>(dmalloc(L->ppart_rows * 2 * 4, L->allocs));
-        L->meta_ints = size_t(3) * T + L->max_segs + L->max_tbl + 4 * size_t(L->max_ditems) +
+        L->meta_ints = size_t(3) * T + L->max_segs + L->max_tbl + kDItemInts * size_t(L->max_ditems) +
                        4 * size_t(L->max_pitems) + 64 +
                        4 * (size_t(L->max_pitems) + 512) + 4;  // prefill work units + combine list
         L->d_meta = static_cast<int32_t*>(dmalloc(L->meta_ints * 4, L->allocs));
@@ -1082,20 +1084,28 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
                 h_slot[row + t] = ss.blocks[p / kBlockTokens] * kBlockTokens + p % kBlockTokens;
             }
             // A short segment (<= kChunkAsDecode tokens: the admitted resume chunk riding in a
-            // decode step) becomes one decode row per token, token t attending keys
-            // 0..start+t: exactly its causal prefix, read through the decode-attention kernel
-            // instead of a small, latency-bound prefill-attention launch (+ combine) per layer.
+            // decode step) goes through the decode-attention kernel as a token group: token t
+            // attends keys 0..start+t (its causal prefix), and its (token, head) columns are
+            // packed 8 per item, so each K/V block is read once per 8 columns instead of a
+            // small, latency-bound prefill-attention launch (+ combine) per layer.
             // DecodeItem.pad = the first position this forward writes for the row's session:
             // blocks from there on are read only after the QKV kernel (PDL wait).
-            static const bool chunk_dec = !(std::getenv("ASB_CHUNK_AS_DECODE") &&
-                                            std::atoi(std::getenv("ASB_CHUNK_AS_DECODE")) == 0);
+            // ASB_CHUNK_AS_DECODE=0: chunks through prefill attention; =2: one item per token
+            // (the unpacked form, for the ablation).
+            static const int chunk_dec = std::getenv("ASB_CHUNK_AS_DECODE")
+                                             ? std::atoi(std::getenv("ASB_CHUNK_AS_DECODE")) : 1;
             constexpr int kChunkAsDecode = 16;
-            // (on small partitions the chunk rows' repeated K/V reads cost more per-SM streaming
-            // than the tensor-core path's one read per tile: decode rows only from 96 SMs,
-            // profiles/r2_chunk_as_decode.txt)
-            if (g.n_tokens == 1 || (chunk_dec && L->n_sms() >= 96 && g.n_tokens <= kChunkAsDecode &&
-                                    int(ditems.size()) + g.n_tokens <= L->max_ditems)) {
-                for (int t = 0; t < g.n_tokens; ++t) ditems.push_back(DecodeItem{row + t, start + t + 1, toff, start});
+            const int G = s.hq / s.hkv;
+            const int n_dit = chunk_dec == 2 ? g.n_tokens : (g.n_tokens * G + 7) / 8;
+            if (g.n_tokens == 1 || (chunk_dec && g.n_tokens <= kChunkAsDecode &&
+                                    int(ditems.size()) + n_dit <= L->max_ditems)) {
+                if (chunk_dec == 2) {
+                    for (int t = 0; t < g.n_tokens; ++t)
+                        ditems.push_back(DecodeItem{row + t, start + t + 1, toff, start, 0, G});
+                } else {
+                    for (int c0 = 0; c0 < g.n_tokens * G; c0 += 8)
+                        ditems.push_back(DecodeItem{row, start + 1, toff, start, c0, g.n_tokens * G});
+                }
                 max_ctx = std::max(max_ctx, start + g.n_tokens);
                 dattn_seg_bytes += double(start + g.n_tokens) * s.hkv * s.hd * 2 * 2;  // K/V read once per session
             } else {
@@ -1113,7 +1123,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         std::memcpy(h_tbl, tbl.data(), tbl.size() * 4);
         int32_t* h_ditems = h_tbl + L->max_tbl;
         std::memcpy(h_ditems, ditems.data(), ditems.size() * sizeof(DecodeItem));
-        int32_t* h_pitems = h_ditems + 4 * L->max_ditems;
+        int32_t* h_pitems = h_ditems + kDItemInts * L->max_ditems;
         std::memcpy(h_pitems, pitems.data(), pitems.size() * sizeof(PrefillItem));
         // prefill work units (one wave, long causal items split; ASB_PREFILL_UNITS=0 off), int4-aligned
         static const bool units_off = std::getenv("ASB_PREFILL_UNITS") && std::atoi(std::getenv("ASB_PREFILL_UNITS")) == 0;
@@ -1137,7 +1147,7 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         const int32_t* d_tbl = d_lrows + L->max_segs;
         const DecodeItem* d_ditems = reinterpret_cast<const DecodeItem*>(d_tbl + L->max_tbl);
         const PrefillItem* d_pitems =
-            reinterpret_cast<const PrefillItem*>(d_tbl + L->max_tbl + 4 * L->max_ditems);
+            reinterpret_cast<const PrefillItem*>(d_tbl + L->max_tbl + kDItemInts * L->max_ditems);
         const int4* d_units = reinterpret_cast<const int4*>(L->d_meta + units_off_ints);
         const int4* d_comb = d_units + punits.size();
 

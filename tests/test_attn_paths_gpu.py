@@ -11,8 +11,9 @@ per process:
   1 split               -> no merge at all on long contexts
   persistent            -> one-wave persistent grid walking (row, kv head, split) units, held-block
                            warp merge, last-arriver split merge incl. empty splits of ragged rows
-the admitted-resume chunk of a decode step through prefill attention (ASB_CHUNK_AS_DECODE=0)
-instead of one causal decode row per chunk token (the default), and both prefill-attention
+the admitted-resume chunk of a decode step through prefill attention (ASB_CHUNK_AS_DECODE=0) or
+as one decode item per token (=2) instead of its (token, head) columns packed 8 per decode item
+(the default, every path above runs it), and both prefill-attention
 decompositions: the default work-unit list (only long causal items
 split, one wave) and the uniform grid.z split (ASB_PREFILL_UNITS=0, optionally forced to 3).
 """
@@ -39,8 +40,10 @@ CASE = "tests/test_forward_gpu.py::test_forward_matches_oracle[hd128-prompt_lens
     {"ASB_DECODE_PERSIST": "1"},
     {"ASB_DECODE_PERSIST": "1", "ASB_DECODE_MAX_SPLITS": "1"},
     {"ASB_CHUNK_AS_DECODE": "0"},
+    {"ASB_CHUNK_AS_DECODE": "2"},
+    {"ASB_CHUNK_AS_DECODE": "2", "ASB_DECODE_PERSIST": "1"},
 ], ids=["cluster3", "last_arriver16", "combine", "single", "prefill_uniform", "prefill_uniform3", "persistent",
-        "persistent_single", "chunk_as_prefill"])
+        "persistent_single", "chunk_as_prefill", "chunk_per_token", "chunk_per_token_persistent"])
 def test_decode_attention_merge_paths(env):
     e = dict(os.environ)
     e.update(env)

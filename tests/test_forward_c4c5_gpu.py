@@ -169,8 +169,9 @@ def test_full_width_truncated_matches_oracle(case):
     {"ASB_PREFILL_UNITS": "0", "ASB_PREFILL_SPLITS": "3"},
     {"ASB_DECODE_PERSIST": "1"},
     {"ASB_TGEMV": "1"},
+    {"ASB_CHUNK_AS_DECODE": "0"},
 ], ids=["cluster3", "last_arriver16", "combine", "single", "prefill_uniform", "prefill_uniform3", "persistent",
-        "tgemv_all"])
+        "tgemv_all", "chunk_as_prefill"])
 def test_c4_layout_merge_paths(env):
     e = dict(os.environ)
     e.update(env)
