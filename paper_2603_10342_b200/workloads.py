@@ -22,6 +22,18 @@ block): t(R) = 1000*B_prof/mu_D(R) is the real step time on R slots,
     theta_high = tau_TPOT, theta_low = tau_TPOT / 2   (the reference's rule, unchanged)
     R_base = R0 = min{R : 1.1 t(R) <= tau_TPOT}   (the R_g* of analysis.cpp:20-32 in step units,
                                                     with 10% co-run headroom)
+The two remaining controller constants get the same treatment (both measured on C3,
+profiles/r2_policy_compare_c3_b0dt*.json):
+    delta_t = 16 isolated full-device steps (C3: 50 ms).  The reference's 250 ms default is a
+              simulator constant; on B200 a C3 cold burst lasts ~0.5-0.8 s, so 250 ms allows two
+              controller moves inside it.  16 steps still averages a dozen step samples per tick.
+    resume budget: an admitted chunk adds chunk_tokens / resume_rate(R_base) to a decode step
+              (the reference's step model, src/executor.cpp:84-97).  If that chunk step misses
+              tau at the base level (with the co-run headroom), admitting resumes into decode
+              steps breaks the SLO the budget protects, so initial_b = b_min = 0: resumes start
+              in Q_P and the budget opens only when TPOT falls below theta_low.
+              (C3: 4.14 + 1.16 ms x 1.1 > 4.71 ms -> 0; TPOT p95/p99 6.6/7.0 -> 5.2/5.6 ms and
+              TTFT p95 481 -> 457 ms over 10 episodes.)
 tau_TTFT keeps the reference's factor-8 calibration.  Virtual-clock runs keep the reference
 model unchanged (they are the decision oracle).
 """
@@ -77,6 +89,10 @@ CORUN = 1.1
 # profiles/r2_prefill_gemm_waves.txt): C3 TTFT p99 -25% and +3% tokens/s for both policies
 # (profiles/r2_policy_compare_c3_unit{2,3,4}.json)
 UNIT_TOKENS = 4096
+# controller interval in isolated full-device decode steps, and the admitted chunk size
+# (executor.resume_chunk_tokens, the reference's default: src/config.cpp)
+CTRL_STEPS = 16
+CHUNK_TOKENS = 16
 
 
 def profile_path(model: str) -> Path:
@@ -107,11 +123,20 @@ def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_fra
     # co-runs and shares HBM / L2, so a level must meet tau with CORUN headroom
     r_base = next((lv for lv in range(1, levels + 1) if step[lv * g] * CORUN <= tau), levels)
     r_base = min(r_base, levels - 1)  # leave the prefill partition at least one slot
+    ctrl = {"theta_high_ms": round(tau, 4), "theta_low_ms": round(theta_low_frac * tau, 4),
+            "r_base_slots": r_base, "initial_r_slots": r_base, "delta_t_ms": round(CTRL_STEPS * t_full, 1)}
+    resume = {int(p["sms"]): float(p["tokens_per_second"]) for p in profile.get("resume_prefill", [])}
+    chunk_ms = None
+    if resume.get(r_base * g):
+        chunk_ms = 1000.0 * CHUNK_TOKENS / resume[r_base * g]
+        if (step[r_base * g] + chunk_ms) * CORUN > tau:
+            ctrl["initial_b_tokens"] = 0
+            ctrl["b_min_tokens"] = 0
     return {"slo": {"tau_tpot_ms": round(tau, 4), "factor": 8.0, "tpot_stat": "p95"},
-            "controller": {"theta_high_ms": round(tau, 4), "theta_low_ms": round(theta_low_frac * tau, 4),
-                           "r_base_slots": r_base, "initial_r_slots": r_base},
+            "controller": ctrl,
             "derived_from": {"decode_batch": B, "decode_ctx": measured.get("decode_ctx"),
                              "full_device_step_ms": round(t_full, 4), "slack": slack,
+                             "chunk_ms_at_base": None if chunk_ms is None else round(chunk_ms, 4),
                              "step_ms_by_level": {lv: round(step[lv * g], 4) for lv in range(1, levels + 1)}}}
 
 

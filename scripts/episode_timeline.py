@@ -28,7 +28,8 @@ cfg = workloads.run_config(a.config, clock=a.clock, policy=pol, lend=bool(kw.get
                            calibrated=bool(kw.get("calib", 1)), slack=float(kw.get("slack", workloads.SLACK)),
                            theta_low_frac=float(kw.get("tlow", 0.5)), static_slots=kw.get("k"),
                            unit_tokens=int(kw.get("unit", workloads.UNIT_TOKENS)))
-for key, ck in (("dt", "delta_t_ms"), ("r0", "initial_r_slots"), ("rbase", "r_base_slots")):
+for key, ck in (("dt", "delta_t_ms"), ("r0", "initial_r_slots"), ("rbase", "r_base_slots"),
+                ("b0", "initial_b_tokens"), ("bmin", "b_min_tokens")):
     if key in kw:
         cfg.setdefault("controller", {})[ck] = kw[key]
 api = Agsv()
@@ -68,12 +69,20 @@ print("metrics", json.dumps({k: m.get(k) for k in ("ttft_p50_ms", "ttft_p95_ms",
 import collections
 by = collections.defaultdict(list)
 for x in steps:
-    by[(x.get("sms", 0), int(x.get("chunk", 0)) > 0)].append(x["t"] - x["start"])
-print(f"{'sms':>4} {'chunk':>5} {'steps':>5} {'p50':>6} {'p95':>6} {'B_avg':>5}")
+    by[(x.get("sms", 0), int(x.get("chunk", 0)) > 0)].append((x["t"] - x["start"], x.get("dev_ms", -1.0)))
+# host = launch -> completion seen by the host; dev = the lane's CUDA-event time of the step
+print(f"{'sms':>4} {'chunk':>5} {'steps':>5} {'host50':>6} {'host95':>6} {'dev50':>6} {'dev95':>6} {'B_avg':>5}")
 for (sms, ch), v in sorted(by.items()):
-    v = sorted(v)
+    h = sorted(a for a, _ in v)
+    d = sorted(b for _, b in v)
     bs = [len(x["emit"]) for x in steps if x.get("sms", 0) == sms and (int(x.get("chunk", 0)) > 0) == ch]
-    print(f"{sms:4d} {str(ch):>5} {len(v):5d} {v[len(v) // 2]:6.2f} {v[int(0.95 * (len(v) - 1))]:6.2f} {sum(bs) / len(bs):5.1f}")
+    print(f"{sms:4d} {str(ch):>5} {len(v):5d} {h[len(h) // 2]:6.2f} {h[int(0.95 * (len(h) - 1))]:6.2f} "
+          f"{d[len(d) // 2]:6.2f} {d[int(0.95 * (len(d) - 1))]:6.2f} {sum(bs) / len(bs):5.1f}")
+# consecutive decode steps: idle time between one step's completion and the next step's launch
+idle = [b["start"] - a["t"] for a, b in zip(steps, steps[1:])]
+idle.sort()
+print("decode lane idle between steps (ms): p50 %.3f p90 %.3f p99 %.3f" % (
+    idle[len(idle) // 2], idle[int(0.9 * (len(idle) - 1))], idle[int(0.99 * (len(idle) - 1))]))
 gaps = []
 prev = {}
 for r in recs:
@@ -82,9 +91,17 @@ for r in recs:
     elif r.get("k") == "step_done":
         for s_ in r["emit"]:
             if prev.get(s_) is not None:
-                gaps.append((r["t"] - prev[s_], r.get("sms", 0), int(r.get("chunk", 0)) > 0, r["t"]))
+                # stalled: the gap holds more than this step (a prefill unit or another step ran between)
+                gaps.append((r["t"] - prev[s_], r.get("sms", 0), int(r.get("chunk", 0)) > 0, r["t"],
+                             (r["t"] - prev[s_]) > (r["t"] - r["start"]) + 0.5))
             prev[s_] = r["t"]
 gaps.sort()
+print("TPOT gap percentiles:", {p: round(gaps[int(p / 100 * (len(gaps) - 1))][0], 2)
+                                for p in (50, 80, 85, 90, 92, 94, 95, 96, 98, 99)})
+for lo in (4.5, 5.0, 6.0):
+    sl = [g for g in gaps if g[0] >= lo]
+    print(f"gaps >= {lo} ms: {len(sl) / len(gaps):.3f} of all; stalled {sum(g[4] for g in sl)}, by (sms, chunk):",
+          dict(collections.Counter((g[1], g[2]) for g in sl)))
 p95 = gaps[int(0.95 * (len(gaps) - 1))][0]
 tail = [g for g in gaps if g[0] >= p95]
 print(f"TPOT gaps {len(gaps)}, p95 {p95:.2f} ms; gaps >= p95: by (sms, chunk):",

@@ -45,3 +45,24 @@ def test_run_configs(name):
     v = workloads.run_config(name, clock="virtual")
     assert "backend" not in v
     json.dumps(cfg)
+
+
+def test_controller_interval_is_sixteen_full_device_steps():
+    prof, meas = _profile([8.6, 4.7, 4.1, 3.15, 3.15, 3.15, 3.15, 3.14, 3.14])
+    assert workloads.calibrate(prof, meas)["controller"]["delta_t_ms"] == pytest.approx(16 * 3.14, abs=0.1)
+
+
+def _with_resume(prof, rate):
+    prof = dict(prof)
+    prof["resume_prefill"] = [{"sms": d["sms"], "tokens_per_second": rate} for d in prof["decode"]]
+    return prof
+
+
+def test_resume_budget_closes_when_a_chunk_step_misses_tau():
+    prof, meas = _profile([8.6, 4.7, 4.1, 3.15, 3.15, 3.15, 3.15, 3.14, 3.14])
+    # base level 3 (4.1 ms); a 16-token chunk at 13.8k tok/s adds 1.16 ms -> 5.8 ms > tau 4.71
+    c = workloads.calibrate(_with_resume(prof, 13800.0), meas)["controller"]
+    assert c["initial_b_tokens"] == 0 == c["b_min_tokens"]
+    # a 0.16 ms chunk fits: the reference's budget defaults stay
+    c = workloads.calibrate(_with_resume(prof, 100000.0), meas)["controller"]
+    assert "initial_b_tokens" not in c and "b_min_tokens" not in c
