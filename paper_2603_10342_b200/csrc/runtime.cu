@@ -1137,7 +1137,13 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
         const size_t used = units_off_ints + 4 * (punits.size() + pcomb.size());
 
         cudaStream_t st = L->stream;
-        cuda_check(cudaEventRecord(L->ev0, st), "event");
+        // ASB_GRAPH_PROBE=1 (measurement only): capture this forward -- meta H2D, every kernel,
+        // ids D2H -- into a CUDA graph and replay it, so ev0..ev1 times the graph-launched step
+        // against the stream-launched one (capture + instantiate happen before ev0).
+        static const bool graph_probe = std::getenv("ASB_GRAPH_PROBE") && std::atoi(std::getenv("ASB_GRAPH_PROBE")) == 1;
+        const bool capture = graph_probe && !L->prof && !L->attn_dbg;
+        if (capture) cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "graph capture");
+        else cuda_check(cudaEventRecord(L->ev0, st), "event");
         cuda_check(cudaMemcpyAsync(L->d_meta, hm, used * 4, cudaMemcpyHostToDevice, st), "meta H2D");
         L->h2d += int64_t(used) * 4;
         const int32_t* d_tok = L->d_meta;
@@ -1317,6 +1323,16 @@ asb_status asb_forward(asb_lane* L, asb_kv* kv, const asb_segment* segs, int n_s
             cudaEvent_t fwd_b = L->take_event();
             cuda_check(cudaEventRecord(fwd_b, st), "event");
             L->marks.push_back(asb_lane::Mark{fwd_a, fwd_b, ASB_STAT_FORWARD, double(T)});
+        }
+        if (capture) {
+            cudaGraph_t g = nullptr;
+            cudaGraphExec_t ge = nullptr;
+            cuda_check(cudaStreamEndCapture(st, &g), "graph end capture");
+            cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+            cuda_check(cudaEventRecord(L->ev0, st), "event");
+            cuda_check(cudaGraphLaunch(ge, st), "graph launch");
+            cuda_check(cudaGraphExecDestroy(ge), "graph destroy");  // deferred until the launch completes
+            cuda_check(cudaGraphDestroy(g), "graph destroy");
         }
         cuda_check(cudaEventRecord(L->ev1, st), "event");
         L->launched = true;
