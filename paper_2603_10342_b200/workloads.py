@@ -109,7 +109,8 @@ def load_profile(model: str) -> tuple[dict | None, dict | None]:
     return doc, meas
 
 
-def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_frac: float = 0.5) -> dict:
+def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_frac: float = 0.5,
+              theta_high_frac: float = 1.0) -> dict:
     """Wall-clock SLO and controller thresholds from the measured decode curve (module doc)."""
     B = int(measured["decode_batch"])
     g = int(profile["granularity"])
@@ -123,7 +124,7 @@ def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_fra
     # co-runs and shares HBM / L2, so a level must meet tau with CORUN headroom
     r_base = next((lv for lv in range(1, levels + 1) if step[lv * g] * CORUN <= tau), levels)
     r_base = min(r_base, levels - 1)  # leave the prefill partition at least one slot
-    ctrl = {"theta_high_ms": round(tau, 4), "theta_low_ms": round(theta_low_frac * tau, 4),
+    ctrl = {"theta_high_ms": round(theta_high_frac * tau, 4), "theta_low_ms": round(theta_low_frac * tau, 4),
             "r_base_slots": r_base, "initial_r_slots": r_base, "delta_t_ms": round(CTRL_STEPS * t_full, 1)}
     resume = {int(p["sms"]): float(p["tokens_per_second"]) for p in profile.get("resume_prefill", [])}
     chunk_ms = None
@@ -143,7 +144,7 @@ def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_fra
 def run_config(name: str, *, clock: str = "wall", policy: str = "agentserve", n_shards: int = 1,
                shard: int = 0, device: int = 0, profile_kernels: bool = False, lend: bool = True,
                calibrated: bool = True, slack: float = SLACK, theta_low_frac: float = 0.5,
-               static_slots: int | None = None, unit_tokens: int = UNIT_TOKENS, seed: int = 13) -> dict:
+               theta_high_frac: float = 1.0, static_slots: int | None = None, unit_tokens: int = UNIT_TOKENS, seed: int = 13) -> dict:
     """agsv_* run config of one BASELINE configuration.  n_shards > 1: this replica serves the
     sessions gid % n_shards == shard of the global agents*n_shards-session workload."""
     c = CONFIGS[name]
@@ -157,7 +158,7 @@ def run_config(name: str, *, clock: str = "wall", policy: str = "agentserve", n_
     if prof is not None:
         cfg["profile"] = {"inline": prof}
         if calibrated and clock != "virtual" and meas is not None:
-            cal = calibrate(prof, meas, slack, theta_low_frac)
+            cal = calibrate(prof, meas, slack, theta_low_frac, theta_high_frac)
             cfg["slo"] = cal["slo"]
             cfg["controller"] = cal["controller"]
     if static_slots is not None:

@@ -8,10 +8,10 @@ attainment, rebind latency and the competitive-ratio verification summary.
       --runs agentserve mixed_fcfs agentserve:lend=0 agentserve:slack=2 static_partition:k=4 \
       --out profiles/r2_policy_compare_c3.json
 
-A run spec is policy[:key=value,...] with keys lend (0/1), slack, tlow (theta_low / tau),
+A run spec is policy[:key=value,...] with keys lend (0/1), slack, tlow (theta_low / tau), thigh (theta_high / tau),
 calib (0/1: measured-curve calibration vs the reference's factor-8), k (static decode slots),
 unit (prefill launch-unit tokens), dt (control interval ms), r0 / rbase (initial / base
-decode slots), b0 / bmin (initial / minimum resume-prefill budget tokens).
+decode slots), b0 / bmin (initial / minimum resume-prefill budget tokens), dr (slots per controller move).
 """
 import argparse
 import json
@@ -64,6 +64,7 @@ def run_spec(api, cfg_name, spec, reps, td, horizon=None):
     cfg = workloads.run_config(cfg_name, policy=pol, lend=bool(kw.get("lend", 1)),
                                calibrated=bool(kw.get("calib", 1)), slack=float(kw.get("slack", workloads.SLACK)),
                                theta_low_frac=float(kw.get("tlow", 0.5)),
+                               theta_high_frac=float(kw.get("thigh", 1.0)),
                                static_slots=kw.get("k"), unit_tokens=int(kw.get("unit", workloads.UNIT_TOKENS)))
     if "dt" in kw:
         cfg.setdefault("controller", {})["delta_t_ms"] = float(kw["dt"])
@@ -71,6 +72,8 @@ def run_spec(api, cfg_name, spec, reps, td, horizon=None):
         cfg.setdefault("controller", {})["initial_r_slots"] = int(kw["r0"])
     if "rbase" in kw:
         cfg.setdefault("controller", {})["r_base_slots"] = int(kw["rbase"])
+    if "dr" in kw:
+        cfg.setdefault("controller", {})["delta_r_slots"] = int(kw["dr"])
     if "b0" in kw:
         cfg.setdefault("controller", {})["initial_b_tokens"] = int(kw["b0"])
     if "bmin" in kw:
