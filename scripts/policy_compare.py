@@ -64,7 +64,7 @@ def run_spec(api, cfg_name, spec, reps, td, horizon=None):
     cfg = workloads.run_config(cfg_name, policy=pol, lend=bool(kw.get("lend", 1)),
                                calibrated=bool(kw.get("calib", 1)), slack=float(kw.get("slack", workloads.SLACK)),
                                theta_low_frac=float(kw.get("tlow", 0.5)),
-                               theta_high_frac=float(kw.get("thigh", 1.0)),
+                               theta_high_frac=float(kw.get("thigh", workloads.THETA_HIGH_FRAC)),
                                static_slots=kw.get("k"), unit_tokens=int(kw.get("unit", workloads.UNIT_TOKENS)))
     if "dt" in kw:
         cfg.setdefault("controller", {})["delta_t_ms"] = float(kw["dt"])
