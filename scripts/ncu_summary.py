@@ -8,6 +8,7 @@ times are cold-cache and serialised, so only each kernel's SHARE is comparable w
 """
 import collections
 import csv
+import gzip
 import io
 import json
 import statistics
@@ -32,7 +33,10 @@ def _short(name):
 
 
 def launches(path):
-    data = [d for d in _rows(open(path).read()) if d.get("Metric Name") == "gpu__time_duration.sum"]
+    opener = gzip.open if path.endswith(".gz") else open
+    with opener(path, "rt") as f:
+        text = f.read()
+    data = [d for d in _rows(text) if d.get("Metric Name") == "gpu__time_duration.sum"]
     scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3}
     agg = collections.defaultdict(list)
     for d in data:
