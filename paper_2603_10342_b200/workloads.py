@@ -25,9 +25,12 @@ block): t(R) = 1000*B_prof/mu_D(R) is the real step time on R slots,
                                                     with 10% co-run headroom)
 The two remaining controller constants get the same treatment (both measured on C3,
 profiles/r2_policy_compare_c3_b0dt*.json):
-    delta_t = 16 isolated full-device steps (C3: 50 ms).  The reference's 250 ms default is a
+    delta_t = 11 isolated full-device steps (C3: 35 ms).  The reference's 250 ms default is a
               simulator constant; on B200 a C3 cold burst lasts ~0.5-0.8 s, so 250 ms allows two
-              controller moves inside it.  16 steps still averages a dozen step samples per tick.
+              controller moves inside it, and when the burst ends the decode batch jumps 7 -> 25
+              rows within ~100 ms (profiles/r2_c3_tail_anatomy_thigh.txt).  11 steps still
+              averages ~8 step samples per tick; 25-50 ms measured, 35 best (TPOT p95 4.59 ms in
+              two 10-episode runs vs 4.86-4.89 at 50 ms, profiles/r2_policy_compare_c3_thigh3/4.json).
     resume budget: an admitted chunk adds chunk_tokens / resume_rate(R_base) to a decode step
               (the reference's step model, src/executor.cpp:84-97).  If that chunk step misses
               tau at the base level (with the co-run headroom), admitting resumes into decode
@@ -92,7 +95,7 @@ CORUN = 1.1
 UNIT_TOKENS = 4096
 # controller interval in isolated full-device decode steps, and the admitted chunk size
 # (executor.resume_chunk_tokens, the reference's default: src/config.cpp)
-CTRL_STEPS = 16
+CTRL_STEPS = 11
 # The controller compares the interval MEAN of the step gaps (scheduler.cpp:55-63) with
 # theta_high while the SLO is on their p95, so theta_high = tau only reacts after the tail has
 # already crossed tau.  Within one partition level the C3 step p50/p95 is 0.84-0.87

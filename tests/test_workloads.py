@@ -50,7 +50,7 @@ def test_run_configs(name):
 
 def test_controller_interval_is_sixteen_full_device_steps():
     prof, meas = _profile([8.6, 4.7, 4.1, 3.15, 3.15, 3.15, 3.15, 3.14, 3.14])
-    assert workloads.calibrate(prof, meas)["controller"]["delta_t_ms"] == pytest.approx(16 * 3.14, abs=0.1)
+    assert workloads.calibrate(prof, meas)["controller"]["delta_t_ms"] == pytest.approx(workloads.CTRL_STEPS * 3.14, abs=0.1)
 
 
 def _with_resume(prof, rate):
