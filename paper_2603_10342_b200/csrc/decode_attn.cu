@@ -777,28 +777,23 @@ cudaError_t launch_hd(const CUtensorMap& tkv, const __nv_bfloat16* q, const Deco
 }  // namespace
 
 int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits) {
-    // Split-KV count minimising the makespan in waves of two resident CTAs per SM: a CTA of
-    // s splits does 1/s of an item's stream, so the cost is ceil(items*s / slots) / s, plus a
-    // small merge charge per extra split.  With items <= slots this is the one-wave rule
-    // (C3 73% -> 84%, C4 84% -> 92% of HBM peak on the full device); on a Green Context
-    // partition it also avoids ragged second waves (128 (row, head) items on a 48-SM
-    // partition: 1 split = 2 waves of full items, 3 splits = 4 waves of 1/3 items = 1.33).
-    // >= 3 blocks (192 keys) per split.
+    // Split-KV count of the one-wave grid (items <= two resident CTAs per SM; larger batches
+    // take the persistent kernel): the most splits that still fit ONE wave, >= 3 blocks (192
+    // keys) per split.  A second wave is never cheaper here: a CTA costs a fixed ~12 us (q
+    // load, ring fill, merge) on top of ~0.5 us per block, so the old makespan-in-waves rule
+    // (which took 5 splits = 4 waves at 80 SMs, 7 at 112 for 128 (row, head) items) ran the
+    // C3 B=16 attention at 53-60 us/layer on 80-112 SM partitions against 37 us with one
+    // split (profiles/r2_decode_attn_levels.txt).
     const int pages = (max_ctx + kBlockTokens - 1) / kBlockTokens;
     const int base = std::max(n_items * hkv, 1);
     const int slots = 2 * std::max(num_sms, 1);
     const int cap = std::max(1, std::min(max_splits, pages / 3));
-    int best = 1;
-    double best_t = 1e30;
-    for (int sp = 1; sp <= cap; ++sp) {
-        const double waves = double((int64_t(base) * sp + slots - 1) / slots);
-        const double t = waves / sp * (1.0 + 0.03 * (sp - 1));
-        if (t < best_t - 1e-9) {
-            best_t = t;
-            best = sp;
-        }
-    }
-    return best;
+    // powers of two only: the split merge runs in a thread-block cluster of `splits` CTAs, and
+    // 5-7 CTA clusters place badly (B=4 on 80-112 SMs: 25 us/layer with 5-7 splits vs 18.5 with
+    // 4 or 8, profiles/r2_decode_attn_levels.txt)
+    int sp = std::max(1, std::min(cap, slots / base));
+    while (sp & (sp - 1)) sp &= sp - 1;
+    return sp;
 }
 
 int decode_splits_persist(int base, int pages, int num_sms, int max_splits) {
@@ -837,7 +832,9 @@ cudaError_t decode_attention(const CUtensorMap& tmap_kv, const __nv_bfloat16* q,
     const bool persist = force <= 0 && persist_env != 0 &&
                          (persist_env == 1 || n_items * s.hkv > 2 * std::max(1, num_sms)) && counters;
     if (persist) {
-        const int sp = decode_splits_persist(n_items * s.hkv, pages, num_sms, max_splits);
+        static const int force_p = std::getenv("ASB_DECODE_PERSIST_SPLITS") ? std::atoi(std::getenv("ASB_DECODE_PERSIST_SPLITS")) : 0;
+        const int sp = force_p > 0 ? std::min(force_p, std::min(max_splits, 16))
+                                   : decode_splits_persist(n_items * s.hkv, pages, num_sms, max_splits);
         const int pps = (pages + sp - 1) / sp;
         const int splits = (pages + pps - 1) / pps;
         if (s.hd == 128)
