@@ -797,20 +797,15 @@ int decode_splits(int n_items, int hkv, int max_ctx, int num_sms, int max_splits
 }
 
 int decode_splits_persist(int base, int pages, int num_sms, int max_splits) {
-    // persistent one-wave grid: makespan = units per CTA x (blocks per unit + per-unit
-    // overhead: q load + warp merge ~1 block, +1 for the split merge)
-    const int slots = 2 * std::max(num_sms, 1);
-    int best = 1;
-    long best_t = -1;
-    for (int sp = 1; sp <= std::min(max_splits, 16); ++sp) {
-        if (sp > 1 && (pages + sp - 1) / sp < 3) break;
-        const long t = (long(base) * sp + slots - 1) / slots * ((pages + sp - 1) / sp + (sp > 1 ? 2 : 1));
-        if (best_t < 0 || t < best_t) {
-            best_t = t;
-            best = sp;
-        }
-    }
-    return best;
+    // The persistent grid runs when the (row, kv head) items already exceed one wave of CTAs, so
+    // splitting KV only adds units, merges and per-unit fills: one split was fastest or tied at
+    // every partition size measured (32-80 SMs, B=24/32 ctx 3000: e.g. 80 SMs B=32 68.8 us/layer
+    // vs 84.7 with the old makespan model's 3 splits, profiles/r2_decode_attn_persist_splits.txt).
+    (void)base;
+    (void)pages;
+    (void)num_sms;
+    (void)max_splits;
+    return 1;
 }
 
 cudaError_t decode_attention(const CUtensorMap& tmap_kv, const __nv_bfloat16* q, const DecodeItem* items,
