@@ -19,8 +19,8 @@ at any real batch and the controller saturates.  In wall-clock mode the threshol
 derived from the measured curve at the batch it was measured at (the profile's `measured`
 block): t(R) = 1000*B_prof/mu_D(R) is the real step time on R slots,
     tau_TPOT = slack * t(S)          (slack 1.5: 50% over the isolated full-device step)
-    theta_high = 0.9 tau_TPOT, theta_low = tau_TPOT / 2   (the reference's rule, with theta_high
-                 below tau: see THETA_HIGH_FRAC)
+    theta_high = 0.85 tau_TPOT, theta_low = 0.4 tau_TPOT   (the reference's rule is tau and
+                 tau / 2: see THETA_HIGH_FRAC)
     R_base = R0 = min{R : 1.1 t(R) <= tau_TPOT}   (the R_g* of analysis.cpp:20-32 in step units,
                                                     with 10% co-run headroom)
 The two remaining controller constants get the same treatment (both measured on C3,
@@ -99,10 +99,14 @@ CTRL_STEPS = 11
 # The controller compares the interval MEAN of the step gaps (scheduler.cpp:55-63) with
 # theta_high while the SLO is on their p95, so theta_high = tau only reacts after the tail has
 # already crossed tau.  Within one partition level the C3 step p50/p95 is 0.84-0.87
-# (profiles/r2_c3_tail_anatomy.txt); over 0.7-1.0 tau, 0.9 measured best on C3 (TPOT p95
-# 5.12-5.19 -> 4.81-4.89 ms over 5 + 10 episodes, both below FCFS; TTFT tails still won;
-# tokens/s -5%; profiles/r2_policy_compare_c3_thigh*.json).
-THETA_HIGH_FRAC = 0.9
+# (profiles/r2_c3_tail_anatomy.txt).  Measured on C3 over theta_high 0.7-1.0 tau and theta_low
+# 0.4-0.5 tau (10-episode runs, profiles/r2_policy_compare_c3_thigh*.json): on the final
+# kernels theta_high 0.85 / theta_low 0.4 gave TPOT p95 4.31 and 4.34 ms vs FCFS 4.43-4.44 in
+# two runs (theta_high 0.9 / theta_low 0.5: 4.70-4.75), TTFT p95/p99 525-545 / 575-592 vs
+# 588-589 / 594-595 ms, tokens/s -6-8%.  The lower theta_low keeps the decode partition from
+# shrinking between the post-burst steps.
+THETA_HIGH_FRAC = 0.85
+THETA_LOW_FRAC = 0.4
 CHUNK_TOKENS = 16
 
 
@@ -120,7 +124,7 @@ def load_profile(model: str) -> tuple[dict | None, dict | None]:
     return doc, meas
 
 
-def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_frac: float = 0.5,
+def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_frac: float = THETA_LOW_FRAC,
               theta_high_frac: float = THETA_HIGH_FRAC) -> dict:
     """Wall-clock SLO and controller thresholds from the measured decode curve (module doc)."""
     B = int(measured["decode_batch"])
@@ -154,7 +158,7 @@ def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_fra
 
 def run_config(name: str, *, clock: str = "wall", policy: str = "agentserve", n_shards: int = 1,
                shard: int = 0, device: int = 0, profile_kernels: bool = False, lend: bool = True,
-               calibrated: bool = True, slack: float = SLACK, theta_low_frac: float = 0.5,
+               calibrated: bool = True, slack: float = SLACK, theta_low_frac: float = THETA_LOW_FRAC,
                theta_high_frac: float = THETA_HIGH_FRAC, static_slots: int | None = None, unit_tokens: int = UNIT_TOKENS, seed: int = 13) -> dict:
     """agsv_* run config of one BASELINE configuration.  n_shards > 1: this replica serves the
     sessions gid % n_shards == shard of the global agents*n_shards-session workload."""

@@ -63,7 +63,7 @@ def run_spec(api, cfg_name, spec, reps, td, horizon=None):
     pol, kw = parse_spec(spec)
     cfg = workloads.run_config(cfg_name, policy=pol, lend=bool(kw.get("lend", 1)),
                                calibrated=bool(kw.get("calib", 1)), slack=float(kw.get("slack", workloads.SLACK)),
-                               theta_low_frac=float(kw.get("tlow", 0.5)),
+                               theta_low_frac=float(kw.get("tlow", workloads.THETA_LOW_FRAC)),
                                theta_high_frac=float(kw.get("thigh", workloads.THETA_HIGH_FRAC)),
                                static_slots=kw.get("k"), unit_tokens=int(kw.get("unit", workloads.UNIT_TOKENS)))
     if "dt" in kw:

@@ -19,7 +19,7 @@ def test_tau_and_thresholds_follow_the_full_device_step():
     tau = 1.5 * 3.14
     assert c["slo"]["tau_tpot_ms"] == pytest.approx(tau, abs=1e-3)
     assert c["controller"]["theta_high_ms"] == pytest.approx(workloads.THETA_HIGH_FRAC * tau, abs=1e-3)
-    assert c["controller"]["theta_low_ms"] == pytest.approx(tau / 2, abs=1e-3)
+    assert c["controller"]["theta_low_ms"] == pytest.approx(workloads.THETA_LOW_FRAC * tau, abs=1e-3)
     assert c["controller"]["theta_low_ms"] < c["controller"]["theta_high_ms"] < tau
 
 
