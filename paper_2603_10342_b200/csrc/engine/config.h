@@ -52,6 +52,10 @@ struct BackendCfg {
     // the full device instead of the decode partition (the idle prefill SMs are lent, and
     // taken back at the next step once prefill work exists)
     bool lend_idle_prefill = false;
+    // Adaptive policies, wall clock: close the control interval early once it holds this many
+    // decode steps whose mean TPOT already exceeds theta_high (the same Algorithm 1 decision,
+    // taken as soon as the evidence is in; the next interval starts then).  0: fixed intervals.
+    int early_tick_steps = 0;
     bool present = false;
     nlohmann::json to_json() const;
 };

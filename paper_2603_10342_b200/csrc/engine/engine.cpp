@@ -230,6 +230,7 @@ private:
             if (!heap_.empty() && heap_.top().t <= t) {
                 const Pending p = heap_.top();
                 heap_.pop();
+                if (p.kind == Kind::Tick && p.gen != tick_gen_) continue;  // superseded by an early tick
                 now_ = t;
                 dispatch(p);
                 continue;
@@ -468,7 +469,18 @@ private:
             anchored_ = false;
         }
         if (mode_ == Mode::Interleaved) last_was_prefill_ = false;
+        if (early_tick_due()) {
+            tick_gen_ += 1;  // the queued tick of this interval is superseded
+            on_tick();       // kicks
+            return;
+        }
         kick();
+    }
+
+    bool early_tick_due() const {
+        const int k = c_.backend.early_tick_steps;
+        return clock_ == Clock::Wall && k > 0 && ctrl_on_ && mode_ == Mode::Partitioned && ctrl_.dk >= k &&
+               ctrl_.dl > c_.ctrl.theta_high * static_cast<double>(ctrl_.dk);
     }
 
     int e_sms(int sms) const { return clock_ == Clock::Wall ? dev_->decode_sms() : sms; }
@@ -717,7 +729,10 @@ private:
             }
         }
         split_ = next;
-        push(static_cast<double>(interval_ + 1) * c_.ctrl.dt, Kind::Tick, 0);
+        if (clock_ == Clock::Wall && c_.backend.early_tick_steps > 0)
+            push(now_ + c_.ctrl.dt, Kind::Tick, 0, tick_gen_);  // intervals restart at early ticks
+        else
+            push(static_cast<double>(interval_ + 1) * c_.ctrl.dt, Kind::Tick, 0);
         kick();
     }
 
@@ -844,6 +859,7 @@ private:
     const Profile& prof_;
     Mode mode_;
     bool ctrl_on_, merge_on_;
+    uint64_t tick_gen_ = 0;  // generation of the queued controller tick (early ticks supersede it)
     Slots slots_;
     Clock clock_;
     std::unique_ptr<DeviceExec> dev_;
