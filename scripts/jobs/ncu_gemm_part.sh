@@ -2,4 +2,3 @@
 ncu --set full --clock-control none --import-source on -k regex:gemm_tn --launch-skip 3 --launch-count 1 \
   -o gpurun_out/ncu_gemm_gu_l2 python scripts/gemm_bench.py --models llama3.2-3b --linears gate_up --tokens 16 --levels 2 --paths 1 --iters 5 > gpurun_out/ncu_gemm.log 2>&1
 ncu -i gpurun_out/ncu_gemm_gu_l2.ncu-rep --page details --csv > gpurun_out/ncu_gemm_gu_l2_details.csv 2>&1
-for t in memcheck racecheck synccheck; do echo "== $t"; timeout 900 compute-sanitizer --tool $t --print-limit 20 python scripts/sanitize_episode.py --quick 2>&1 | tail -6; done

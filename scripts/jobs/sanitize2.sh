@@ -1,3 +1,4 @@
+# NOTE: compute-sanitizer has since been closed on the GPU pool (runs under it left GPUs needing a reset); kept as the record of how r2_compute_sanitizer*.txt were produced
 # compute-sanitizer over the packed-chunk decode attention (hd128, G=3 columns spanning tokens) and
 # the per-token / persistent variants, plus the quick episodes (tiny model, G=2 chunks)
 CS=/usr/local/cuda/bin/compute-sanitizer
