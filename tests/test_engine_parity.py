@@ -193,3 +193,19 @@ def test_verify_error_statuses_match(apis, params):
         rep = ctypes.c_void_p()
         sts.append(api.L.agsv_verify_trace(t.h, params.encode(), ctypes.byref(rep)))
     assert sts[0] == sts[1] and sts[0] != 0
+
+
+def test_early_tick_is_wall_clock_only(apis, tmp):
+    """backend.early_tick_steps (wall-clock early controller tick) is validated, and a virtual
+    run that sets it records the same events, byte for byte, as the reference's run without it
+    (only the config header line, which echoes the backend section, differs)."""
+    mine, ref = apis
+    cfg = {"workload": {"paradigm": "react", "concurrency": 6}, "policy": "agentserve", "seed": 13}
+    with pytest.raises(AgsvError):
+        mine.config(json.dumps({**cfg, "backend": {"clock": "virtual", "early_tick_steps": -1}}))
+    a = mine.run({**cfg, "backend": {"clock": "virtual", "early_tick_steps": 3}})
+    b = ref.run(cfg)
+    assert a.workload_hash == b.workload_hash
+    la, lb = a.jsonl(tmp).splitlines(), b.jsonl(tmp).splitlines()
+    assert len(la) == len(lb) > 10
+    assert la[1:] == lb[1:]
