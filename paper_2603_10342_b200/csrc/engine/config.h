@@ -56,6 +56,10 @@ struct BackendCfg {
     // decode steps whose mean TPOT already exceeds theta_high (the same Algorithm 1 decision,
     // taken as soon as the evidence is in; the next interval starts then).  0: fixed intervals.
     int early_tick_steps = 0;
+    // Adaptive policies, wall clock: theta_high used while Q_P holds no cold prefill (only
+    // resume prefills, or none), when prefill SMs cost little TTFT; the controller's
+    // theta_high applies during cold bursts.  0: the controller's theta_high throughout.
+    double theta_high_no_cold_ms = 0.0;
     bool present = false;
     nlohmann::json to_json() const;
 };

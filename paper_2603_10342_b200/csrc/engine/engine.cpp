@@ -477,6 +477,17 @@ private:
         kick();
     }
 
+    // Controller constants of this tick: backend.theta_high_no_cold_ms replaces theta_high
+    // (wall clock) while no cold prefill is queued or running.
+    CtrlCfg tick_ctrl() const {
+        CtrlCfg k = c_.ctrl;
+        const double th = c_.backend.theta_high_no_cold_ms;
+        if (clock_ == Clock::Wall && th > k.theta_low &&
+            std::none_of(qp_.begin(), qp_.end(), [](const Job& j) { return j.kind == ReqKind::Cold; }))
+            k.theta_high = th;
+        return k;
+    }
+
     bool early_tick_due() const {
         const int k = c_.backend.early_tick_steps;
         return clock_ == Clock::Wall && k > 0 && ctrl_on_ && mode_ == Mode::Partitioned && ctrl_.dk >= k &&
@@ -701,7 +712,7 @@ private:
         s.starved = acct_starved_;
         const auto tpot = take_tpot(ctrl_);
         s.tpot = tpot.value_or(-1.0);
-        if (ctrl_on_ && tpot) ctrl_ = ctrl_step(ctrl_, *tpot, c_.ctrl);
+        if (ctrl_on_ && tpot) ctrl_ = ctrl_step(ctrl_, *tpot, tick_ctrl());
         s.b = ctrl_.b;
         s.r = ctrl_.r;
         Event te = ev(Ev::Tick, t);

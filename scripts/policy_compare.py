@@ -11,7 +11,7 @@ attainment, rebind latency and the competitive-ratio verification summary.
 A run spec is policy[:key=value,...] with keys lend (0/1), slack, tlow (theta_low / tau), thigh (theta_high / tau),
 calib (0/1: measured-curve calibration vs the reference's factor-8), k (static decode slots),
 unit (prefill launch-unit tokens), dt (control interval ms), r0 / rbase (initial / base
-decode slots), b0 / bmin (initial / minimum resume-prefill budget tokens), dr (slots per controller move), early (backend.early_tick_steps).
+decode slots), b0 / bmin (initial / minimum resume-prefill budget tokens), dr (slots per controller move), early (backend.early_tick_steps), thnc (backend.theta_high_no_cold_ms / tau).
 """
 import argparse
 import json
@@ -72,6 +72,8 @@ def run_spec(api, cfg_name, spec, reps, td, horizon=None):
         cfg.setdefault("controller", {})["initial_r_slots"] = int(kw["r0"])
     if "rbase" in kw:
         cfg.setdefault("controller", {})["r_base_slots"] = int(kw["rbase"])
+    if "thnc" in kw:  # theta_high while no cold prefill is queued, as a fraction of tau
+        cfg.setdefault("backend", {})["theta_high_no_cold_ms"] = round(float(kw["thnc"]) * cfg["slo"]["tau_tpot_ms"], 4)
     if "early" in kw:
         cfg.setdefault("backend", {})["early_tick_steps"] = int(kw["early"])
     if "dr" in kw:

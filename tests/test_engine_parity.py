@@ -196,14 +196,16 @@ def test_verify_error_statuses_match(apis, params):
 
 
 def test_early_tick_is_wall_clock_only(apis, tmp):
-    """backend.early_tick_steps (wall-clock early controller tick) is validated, and a virtual
+    """backend.early_tick_steps (wall-clock early controller tick) and theta_high_no_cold_ms
+    are validated, and a virtual
     run that sets it records the same events, byte for byte, as the reference's run without it
     (only the config header line, which echoes the backend section, differs)."""
     mine, ref = apis
     cfg = {"workload": {"paradigm": "react", "concurrency": 6}, "policy": "agentserve", "seed": 13}
-    with pytest.raises(AgsvError):
-        mine.config(json.dumps({**cfg, "backend": {"clock": "virtual", "early_tick_steps": -1}}))
-    a = mine.run({**cfg, "backend": {"clock": "virtual", "early_tick_steps": 3}})
+    for bad in ({"early_tick_steps": -1}, {"theta_high_no_cold_ms": -1.0}):
+        with pytest.raises(AgsvError):
+            mine.config(json.dumps({**cfg, "backend": {"clock": "virtual", **bad}}))
+    a = mine.run({**cfg, "backend": {"clock": "virtual", "early_tick_steps": 3, "theta_high_no_cold_ms": 30.0}})
     b = ref.run(cfg)
     assert a.workload_hash == b.workload_hash
     la, lb = a.jsonl(tmp).splitlines(), b.jsonl(tmp).splitlines()
