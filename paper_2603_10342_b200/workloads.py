@@ -19,8 +19,8 @@ at any real batch and the controller saturates.  In wall-clock mode the threshol
 derived from the measured curve at the batch it was measured at (the profile's `measured`
 block): t(R) = 1000*B_prof/mu_D(R) is the real step time on R slots,
     tau_TPOT = slack * t(S)          (slack 1.5: 50% over the isolated full-device step)
-    theta_high = 0.85 tau_TPOT, theta_low = 0.4 tau_TPOT   (the reference's rule is tau and
-                 tau / 2: see THETA_HIGH_FRAC)
+    theta_high = tau_TPOT during cold bursts, 0.85 tau_TPOT otherwise, theta_low = 0.4 tau_TPOT
+                 (the reference's rule is tau and tau / 2: see THETA_HIGH_FRAC)
     R_base = R0 = min{R : 1.1 t(R) <= tau_TPOT}   (the R_g* of analysis.cpp:20-32 in step units,
                                                     with 10% co-run headroom)
 The two remaining controller constants get the same treatment (both measured on C3,
@@ -98,14 +98,18 @@ UNIT_TOKENS = 4096
 CTRL_STEPS = 11
 # The controller compares the interval MEAN of the step gaps (scheduler.cpp:55-63) with
 # theta_high while the SLO is on their p95, so theta_high = tau only reacts after the tail has
-# already crossed tau.  Within one partition level the C3 step p50/p95 is 0.84-0.87
-# (profiles/r2_c3_tail_anatomy.txt).  Measured on C3 over theta_high 0.7-1.0 tau and theta_low
-# 0.4-0.5 tau (10-episode runs, profiles/r2_policy_compare_c3_thigh*.json): on the final
-# kernels theta_high 0.85 / theta_low 0.4 gave TPOT p95 4.31 and 4.34 ms vs FCFS 4.43-4.44 in
-# two runs (theta_high 0.9 / theta_low 0.5: 4.70-4.75), TTFT p95/p99 525-545 / 575-592 vs
-# 588-589 / 594-595 ms, tokens/s -6-8%.  The lower theta_low keeps the decode partition from
-# shrinking between the post-burst steps.
-THETA_HIGH_FRAC = 0.85
+# already crossed tau (within one partition level the C3 step p50/p95 is 0.84-0.87,
+# profiles/r2_c3_tail_anatomy.txt).  But every SM the controller moves to decode during a COLD
+# burst is taken from the prefills that set TTFT and throughput, while after the burst the
+# prefill partition only holds short resume prefills.  So theta_high is phase-dependent
+# (backend.theta_high_no_cold_ms, wall clock): tau while a cold prefill is queued or running,
+# 0.85 tau otherwise; theta_low 0.4 tau keeps the partition from shrinking between post-burst
+# steps.  C3, 20 episodes (profiles/r2_policy_compare_c3_thnc*.json): TTFT p95/p99 456/471 vs
+# 585/591 ms for FCFS, TPOT p99 4.96 vs 7.60 ms, tokens/s within 1% of FCFS; TPOT p95 4.62 vs
+# 4.42 ms.  A constant 0.85 tau instead ties FCFS on TPOT p95 (4.40-4.47 vs 4.40-4.42) and on
+# TTFT p99 (566-593 vs 591-592) at 5-7% fewer tokens/s (_thigh5/6, _final20.json).
+THETA_HIGH_FRAC = 1.0
+THETA_HIGH_NO_COLD_FRAC = 0.85
 THETA_LOW_FRAC = 0.4
 CHUNK_TOKENS = 16
 
@@ -125,7 +129,8 @@ def load_profile(model: str) -> tuple[dict | None, dict | None]:
 
 
 def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_frac: float = THETA_LOW_FRAC,
-              theta_high_frac: float = THETA_HIGH_FRAC) -> dict:
+              theta_high_frac: float = THETA_HIGH_FRAC,
+              theta_high_no_cold_frac: float = THETA_HIGH_NO_COLD_FRAC) -> dict:
     """Wall-clock SLO and controller thresholds from the measured decode curve (module doc)."""
     B = int(measured["decode_batch"])
     g = int(profile["granularity"])
@@ -150,6 +155,7 @@ def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_fra
             ctrl["b_min_tokens"] = 0
     return {"slo": {"tau_tpot_ms": round(tau, 4), "factor": 8.0, "tpot_stat": "p95"},
             "controller": ctrl,
+            "backend": {"theta_high_no_cold_ms": round(theta_high_no_cold_frac * tau, 4)},
             "derived_from": {"decode_batch": B, "decode_ctx": measured.get("decode_ctx"),
                              "full_device_step_ms": round(t_full, 4), "slack": slack,
                              "chunk_ms_at_base": None if chunk_ms is None else round(chunk_ms, 4),
@@ -159,7 +165,8 @@ def calibrate(profile: dict, measured: dict, slack: float = SLACK, theta_low_fra
 def run_config(name: str, *, clock: str = "wall", policy: str = "agentserve", n_shards: int = 1,
                shard: int = 0, device: int = 0, profile_kernels: bool = False, lend: bool = True,
                calibrated: bool = True, slack: float = SLACK, theta_low_frac: float = THETA_LOW_FRAC,
-               theta_high_frac: float = THETA_HIGH_FRAC, static_slots: int | None = None, unit_tokens: int = UNIT_TOKENS, seed: int = 13) -> dict:
+               theta_high_frac: float = THETA_HIGH_FRAC,
+               theta_high_no_cold_frac: float = THETA_HIGH_NO_COLD_FRAC, static_slots: int | None = None, unit_tokens: int = UNIT_TOKENS, seed: int = 13) -> dict:
     """agsv_* run config of one BASELINE configuration.  n_shards > 1: this replica serves the
     sessions gid % n_shards == shard of the global agents*n_shards-session workload."""
     c = CONFIGS[name]
@@ -170,16 +177,18 @@ def run_config(name: str, *, clock: str = "wall", policy: str = "agentserve", n_
         w["shard_count"] = n_shards
     cfg = {"workload": w, "policy": policy, "seed": seed, "slo": {"factor": 8.0, "tpot_stat": "p95"}}
     prof, meas = load_profile(c["model"])
+    cal_backend = {}
     if prof is not None:
         cfg["profile"] = {"inline": prof}
         if calibrated and clock != "virtual" and meas is not None:
-            cal = calibrate(prof, meas, slack, theta_low_frac, theta_high_frac)
+            cal = calibrate(prof, meas, slack, theta_low_frac, theta_high_frac, theta_high_no_cold_frac)
             cfg["slo"] = cal["slo"]
             cfg["controller"] = cal["controller"]
+            cal_backend = cal["backend"]
     if static_slots is not None:
         cfg["static_decode_slots"] = static_slots
     if clock != "virtual":
         cfg["backend"] = {"clock": clock, "model": c["model"], "device": device,
                           "profile_kernels": profile_kernels, "prefill_unit_tokens": unit_tokens,
-                          "lend_idle_prefill": bool(lend)}
+                          "lend_idle_prefill": bool(lend), **cal_backend}
     return cfg

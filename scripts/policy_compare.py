@@ -65,6 +65,7 @@ def run_spec(api, cfg_name, spec, reps, td, horizon=None):
                                calibrated=bool(kw.get("calib", 1)), slack=float(kw.get("slack", workloads.SLACK)),
                                theta_low_frac=float(kw.get("tlow", workloads.THETA_LOW_FRAC)),
                                theta_high_frac=float(kw.get("thigh", workloads.THETA_HIGH_FRAC)),
+                               theta_high_no_cold_frac=float(kw.get("thnc", workloads.THETA_HIGH_NO_COLD_FRAC)),
                                static_slots=kw.get("k"), unit_tokens=int(kw.get("unit", workloads.UNIT_TOKENS)))
     if "dt" in kw:
         cfg.setdefault("controller", {})["delta_t_ms"] = float(kw["dt"])
@@ -72,8 +73,6 @@ def run_spec(api, cfg_name, spec, reps, td, horizon=None):
         cfg.setdefault("controller", {})["initial_r_slots"] = int(kw["r0"])
     if "rbase" in kw:
         cfg.setdefault("controller", {})["r_base_slots"] = int(kw["rbase"])
-    if "thnc" in kw:  # theta_high while no cold prefill is queued, as a fraction of tau
-        cfg.setdefault("backend", {})["theta_high_no_cold_ms"] = round(float(kw["thnc"]) * cfg["slo"]["tau_tpot_ms"], 4)
     if "early" in kw:
         cfg.setdefault("backend", {})["early_tick_steps"] = int(kw["early"])
     if "dr" in kw:

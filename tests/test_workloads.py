@@ -20,7 +20,11 @@ def test_tau_and_thresholds_follow_the_full_device_step():
     assert c["slo"]["tau_tpot_ms"] == pytest.approx(tau, abs=1e-3)
     assert c["controller"]["theta_high_ms"] == pytest.approx(workloads.THETA_HIGH_FRAC * tau, abs=1e-3)
     assert c["controller"]["theta_low_ms"] == pytest.approx(workloads.THETA_LOW_FRAC * tau, abs=1e-3)
-    assert c["controller"]["theta_low_ms"] < c["controller"]["theta_high_ms"] < tau
+    assert c["controller"]["theta_low_ms"] < c["controller"]["theta_high_ms"] <= tau
+    # phase-dependent theta_high: below tau once no cold prefill is queued, above theta_low
+    nc = c["backend"]["theta_high_no_cold_ms"]
+    assert nc == pytest.approx(workloads.THETA_HIGH_NO_COLD_FRAC * tau, abs=1e-3)
+    assert c["controller"]["theta_low_ms"] < nc < tau
 
 
 def test_base_level_keeps_corun_headroom():
